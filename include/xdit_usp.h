@@ -1,0 +1,237 @@
+/*
+ * xdit_usp.h -- C ABI of libxdit_usp.so, the B200 (sm_100a) USP attention hot path of xDiT
+ * (arXiv 2411.01738).  PAPER.md = /root/reference/PAPER.md (cited as P:<line> §<section>).
+ *
+ * The operation: full (non-causal) multi-head attention softmax(Q K^T / sqrt(D)) V over the joint
+ * [text; image] token sequence of a DiT block ("full attention" P:257 §4.1.2; joint sequence
+ * P:185-187 §3, §4.1.1), sharded by Unified Sequence Parallelism: a 2D mesh "where the
+ * columns are SP-Ring groups and rows are SP-Ulysses groups" (§4.1.4).  Ulysses
+ * "employs All2All communications to transform the partitioning along the sequence dimension into
+ * partitioning along the head dimension" (§4.1.1); Ring is "a parallel version of Flash
+ * Attention ... utilizing peer-to-peer (P2P) transmission of K and V subblock" (§4.1.1),
+ * whose per-block partial results are merged by log-sum-exp.  CFG parallelism (§4.2) is
+ * an outer batch split: the caller builds one communicator per CFG group and passes that group's
+ * batch; nothing in this ABI sees it.
+ *
+ * Conventions (every function):
+ *   - Return value: XDIT_OK (0) or an xdit_status code; the library never aborts.  The message of
+ *     the last non-OK return on the calling thread is xdit_last_error().
+ *   - Tensor pointers are DEVICE pointers owned by the caller (e.g. torch tensors) unless stated.
+ *     The library never frees, retains or allocates caller memory; it allocates only inside
+ *     xdit_comm_reserve (workspace owned by the comm handle).
+ *   - All enqueueing functions are stream-ordered on the caller's `stream` and return without a
+ *     host synchronisation; results are valid when `stream` reaches the enqueue point.
+ *   - Scale is fixed to 1/sqrt(D) with the true head dim D (reading C1).  LSE is the
+ *     natural log of sum_j exp(scaled logit_j), fp32 (reading C2).
+ *   - bf16 = IEEE bfloat16 stored as uint16; fp32 = IEEE binary32.
+ *   - Global joint sequence order is [text; image] (reading C4); S = S_txt + S_img.
+ */
+#ifndef XDIT_USP_H
+#define XDIT_USP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define XDIT_API __attribute__((visibility("default")))
+#else
+#define XDIT_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct xdit_comm_s* xdit_comm_t; /* opaque: mesh, NCCL sub-communicators, workspace */
+typedef struct CUstream_st* xdit_stream_t; /* == cudaStream_t; NULL = legacy default stream */
+
+typedef enum xdit_status {
+  XDIT_OK = 0,
+  XDIT_ERR_INVALID_ARG = 1,   /* null pointer, non-positive size, mismatched scalars */
+  XDIT_ERR_UNSUPPORTED = 2,   /* head dim or dtype not supported by this entry point */
+  XDIT_ERR_DIVISIBILITY = 3,  /* H % ulysses != 0 -- P:541 "16 does not divide evenly into 24" */
+  XDIT_ERR_COMM_MISMATCH = 4, /* ulysses*ring != comm size, or (u,r) differs from the handle's */
+  XDIT_ERR_EMPTY_SHARD = 5,   /* some rank would hold zero tokens (reading C5) */
+  XDIT_ERR_ALIGNMENT = 6,     /* pointer not 16-byte aligned or row bytes not a multiple of 16 */
+  XDIT_ERR_CUDA = 7,          /* a CUDA runtime/driver call failed (message has the name) */
+  XDIT_ERR_NCCL = 8,          /* an NCCL call failed, or an async NCCL error was pending */
+  XDIT_ERR_WORKSPACE = 9      /* problem exceeds the reservation made by xdit_comm_reserve */
+} xdit_status;
+
+/* Thread-local, NUL-terminated message for the last non-OK return ("" if none).  Valid until the
+ * next call on the same thread.  Never NULL. */
+XDIT_API const char* xdit_last_error(void);
+
+/* Library ABI version (major*10000 + minor*100 + patch). */
+XDIT_API int xdit_version(void);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Shard rule (§4.1.1; reading C5).  In-context conditioning: "splits both the        */
+/* Condition Tensor and Image Tensor along the sequence dimension. Then, it concatenates        */
+/* corresponding shards of condition and image input to form a local sequence."                 */
+/* Text and image are split separately into nranks balanced contiguous pieces: piece g has      */
+/* floor(S/n) + (g < S mod n) tokens (np.array_split convention).  Rank g's local sequence is   */
+/* concat(text piece g, image piece g), S_loc = *txt_len + *img_len.  Pure host function.       */
+/* Errors: INVALID_ARG (negative sizes, nranks<1, g out of range); EMPTY_SHARD if S_loc == 0.    */
+/* Outputs are written even for EMPTY_SHARD.                                                    */
+/* ------------------------------------------------------------------------------------------ */
+XDIT_API int xdit_usp_shard(int S_txt, int S_img, int nranks, int g, int* txt_off, int* txt_len,
+                   int* img_off, int* img_len);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Communicators.  One handle per SP group (= one CFG group).  Mesh (reading C6): SP rank  */
+/* g = i*ulysses + j, i = ring index (SP-Ring column), j = Ulysses index (SP-Ulysses row).  The  */
+/* handle owns two NCCL sub-communicators split from the SP communicator: Ulysses (color i,     */
+/* key j) and Ring (color j, key i), plus all workspace.                                        */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Writes a fresh NCCL unique id (an opaque 128-byte blob) to id_out (HOST memory, >=128 bytes).
+ * Rank 0 of the SP group calls it and broadcasts the bytes to the other ranks (e.g. with
+ * torch.distributed), which then call xdit_comm_init.  Errors: INVALID_ARG, NCCL. */
+XDIT_API int xdit_nccl_unique_id(void* id_out);
+
+/* Collective over the nranks = ulysses*ring ranks of one SP group: builds the SP communicator
+ * from `unique_id` (HOST, 128 bytes) on the current CUDA device, then splits the Ulysses and
+ * Ring sub-communicators.  With nranks == 1, unique_id may be NULL and no NCCL object is made.
+ * Errors: INVALID_ARG, COMM_MISMATCH (ulysses*ring != nranks), NCCL, CUDA. */
+XDIT_API int xdit_comm_init(const void* unique_id, int nranks, int rank, int ulysses, int ring,
+                   xdit_comm_t* out);
+
+/* Same as xdit_comm_init but wraps an existing ncclComm_t of the SP group (for example one a
+ * framework already owns, NCCL 2.28.x ABI).  The handle does not take ownership of nccl_comm.
+ * nccl_comm may be NULL only when ulysses*ring == 1. */
+XDIT_API int xdit_comm_create(void* nccl_comm, int ulysses, int ring, xdit_comm_t* out);
+
+/* Allocates (or grows) the device workspace for a problem: Ulysses send/recv buffers, the
+ * unpacked Q block, two ring KV slots, fp32 ring accumulators.  Call once per shape before the
+ * hot loop (all ranks, same scalars); xdit_usp_attention never allocates, so the call path is
+ * CUDA-graph capturable.  elem_bytes = 2 (bf16 path) or 4 (fp32 path).  S_txt/S_img are
+ * GLOBAL token counts.  Errors: INVALID_ARG, DIVISIBILITY, EMPTY_SHARD, UNSUPPORTED, CUDA. */
+XDIT_API int xdit_comm_reserve(xdit_comm_t comm, int B, int H, int S_txt, int S_img, int D, int elem_bytes);
+
+/* Reports the handle's mesh.  Any output pointer may be NULL. */
+XDIT_API int xdit_comm_info(xdit_comm_t comm, int* nranks, int* rank, int* ulysses, int* ring);
+
+/* Frees the workspace and the NCCL objects the handle created (device-synchronising).
+ * NULL is accepted and ignored. */
+XDIT_API int xdit_comm_destroy(xdit_comm_t comm);
+
+/* Per-rank geometry of one USP call, as the library will execute it (pure host function; all
+ * ranks compute identical plans from identical scalars).  Exposed so host logic can be checked
+ * without a GPU (e.g. multi-process gloo tests).  Ring step s uses the KV block of ring index
+ * ring_src[s] = (i - s) mod ring (reading C9) with ring_rows[s] keys; the Ulysses exchange pads
+ * every shard to Lmax rows; seg_off[] are this rank's ring-block row offsets of its Ulysses peers'
+ * shards (one segment per peer, reading C6/C7). */
+typedef struct xdit_plan {
+  int32_t nranks, rank, ulysses, ring;
+  int32_t i, j;        /* ring index (column) and Ulysses index (row) of `rank` */
+  int32_t Hh;          /* heads per Ulysses rank = H / ulysses */
+  int32_t S_loc;       /* tokens held by `rank` (= txt_len + img_len) */
+  int32_t Lmax;        /* max S_loc over the SP group (a2a padding) */
+  int32_t S_blk;       /* rows of this rank's ring block (queries after the Ulysses a2a) */
+  int32_t ring_next, ring_prev;      /* ring-communicator ranks this rank sends to / receives from */
+  int32_t nseg, seg_off[9];          /* ring-block rows contributed by Ulysses peer p: [off[p], off[p+1]) */
+  int32_t ring_src[8], ring_rows[8]; /* per ring step s < ring */
+  int64_t a2a_bytes_per_peer;        /* Q,K,V exchange chunk (bf16 elements x 2 bytes) */
+  int64_t ring_bytes[8];             /* K+V bytes sent at step s (0 on the last step) */
+} xdit_plan;
+XDIT_API int xdit_usp_plan(int B, int H, int S_txt, int S_img, int D, int ulysses, int ring,
+                           int rank, xdit_plan* out);
+
+/* ------------------------------------------------------------------------------------------ */
+/* The hot path: one USP attention call.                                 */
+/*                                                                                              */
+/* q, k, v, out : this rank's local tokens, [B][S_loc][H][D] contiguous, bf16; S_loc from        */
+/*                xdit_usp_shard(S_txt, S_img, ulysses*ring, rank).  16-byte aligned.            */
+/* lse          : fp32 [B][H][S_loc] (natural log) or NULL to skip (reading C15).               */
+/* B, H, D      : batch of this SP (CFG) group, heads, head dim.  D in {64, 128} (UNSUPPORTED    */
+/*                otherwise; the fp32 entry point takes any D in [1, 256]).                     */
+/* S_txt, S_img : GLOBAL text / image token counts of the joint sequence.                       */
+/* ulysses,ring : degrees; must equal the handle's; H % ulysses == 0 (DIVISIBILITY).             */
+/* stream       : caller's CUDA stream; an internal side stream carries NCCL and is joined back. */
+/* comm         : handle from xdit_comm_init/create, reserved for this shape (WORKSPACE).        */
+/*                                                                                              */
+/* Steps: pack Q,K,V by head block -> Ulysses all-to-all -> unpack to the ring    */
+/* block -> r ring steps {attention on the current KV block (tcgen05 kernel) || send/recv of the */
+/* next KV block; LSE merge} -> bf16 cast + pack by destination -> reverse all-to-all of O and   */
+/* LSE -> unpack into out/lse.  Invalid arguments are rejected before anything is enqueued, so a */
+/* failing rank never leaves a peer hanging inside a collective (all ranks must pass identical  */
+/* scalars).  Not re-entrant per handle.  Deterministic run to run for a fixed (ulysses, ring). */
+/* ------------------------------------------------------------------------------------------ */
+XDIT_API int xdit_usp_attention(const void* q, const void* k, const void* v, void* out, float* lse, int B,
+                       int H, int S_txt, int S_img, int D, int ulysses, int ring,
+                       xdit_stream_t stream, xdit_comm_t comm);
+
+/* fp32-input mode: identical contract with fp32 q, k, v, out; SIMT fp32 arithmetic throughout
+ * (no tensor cores), any D in [1, 256] with D*4 a multiple of 16 bytes when ulysses*ring > 1. */
+XDIT_API int xdit_usp_attention_f32(const float* q, const float* k, const float* v, float* out, float* lse,
+                           int B, int H, int S_txt, int S_img, int D, int ulysses, int ring,
+                           xdit_stream_t stream, xdit_comm_t comm);
+
+/* ------------------------------------------------------------------------------------------ */
+/* Stage entry points (single device).  xdit_usp_attention is composed of exactly these          */
+/* launches plus NCCL; they are exported so a single GPU can drive every (ulysses, ring) split   */
+/* as virtual ranks in tests.  All strides are in ELEMENTS; the innermost (d) stride is 1.       */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Destination map of an output row block (used where a kernel writes O and LSE).  Block row t
+ * belongs to segment s with seg_off[s] <= t < seg_off[s+1] (nseg in [1,8], seg_off[0] = 0,
+ * seg_off[nseg] = number of rows); its element (b, t, h, d) goes to
+ *   o + s*o_seg + b*o_b + (t - seg_off[s])*o_s + h*o_h + d
+ * and its LSE (b, h, t) to  lse + s*l_seg + b*l_b + h*l_h + (t - seg_off[s]).
+ * A single segment with o_seg = l_seg = 0 is a plain strided tensor.  This lets the final
+ * epilogue write straight into the reverse all-to-all send buffer (one segment per Ulysses peer). */
+typedef struct xdit_rowmap {
+  int32_t nseg;
+  int32_t seg_off[9];
+  int64_t o_seg, o_b, o_s, o_h;
+  int64_t l_seg, l_b, l_h;
+} xdit_rowmap;
+
+/* Flash attention forward of one (Q block, KV block) pair -- SURVEY §8(a) step a6.
+ * q: [B][Sq][H][D] with strides (q_b, q_s, q_h); k, v: [B][Skv][H][D] with strides
+ * (kv_b, kv_s, kv_h) shared by k and v.  dtype: 0 = bf16 inputs on the tcgen05/TMEM/TMA kernel
+ * (D in {64,128}; q,k,v 16-byte aligned, strides multiples of 8 elements), 1 = fp32 inputs on the
+ * SIMT kernel (D in [1,256]).  out_f32: 0 writes O as bf16 through `omap` (final output);
+ * 1 writes O as fp32 through `omap` (ring partial).  lse may be NULL (skipped).
+ * Errors: INVALID_ARG, UNSUPPORTED, ALIGNMENT, CUDA. */
+XDIT_API int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,
+                  int Sq, int Skv, int D, int64_t q_b, int64_t q_s, int64_t q_h, int64_t kv_b,
+                  int64_t kv_s, int64_t kv_h, const xdit_rowmap* omap, int dtype, int out_f32,
+                  xdit_stream_t stream);
+
+/* Ring partial-output merge ("parallel version of Flash Attention").
+ * o_acc, o_s: fp32 [B][S][Hh][D] contiguous; lse_acc, lse_s: fp32 [B][Hh][S].
+ *   L = M + log(exp(lse_acc - M) + exp(lse_s - M)), M = max(lse_acc, lse_s)
+ *   O = exp(lse_acc - L) * o_acc + exp(lse_s - L) * o_s
+ * If final == NULL: O, L overwrite o_acc, lse_acc.  Else the merged O is cast (RNE) to
+ * final_dtype (0 bf16, 1 fp32) and written with L through *final_map into `final` / `final_lse`
+ * (final_lse may be NULL).  Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_lse_merge(float* o_acc, float* lse_acc, const float* o_s, const float* lse_s, int B, int S,
+                   int Hh, int D, void* final, float* final_lse, const xdit_rowmap* final_map,
+                   int final_dtype, xdit_stream_t stream);
+
+/* Ulysses pack: x [B][L][H][D] (contiguous, elem_bytes each) ->
+ * send[p][t][B][Lmax][H/u][D] for p in [0,u) with t = `slot` of `nslots`, i.e. head block p of
+ * every local token into peer p's contiguous chunk.  Rows L..Lmax-1 are left untouched.
+ * Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u, int slot,
+                  int nslots, int elem_bytes, xdit_stream_t stream);
+
+/* Ulysses unpack: recv[p][t][B][Lmax][Hh][D] (slot t of nslots) ->
+ * y[B][S_blk][Hh][D] with y rows = concat over p of the first len[p] rows of peer p's chunk
+ * (S_blk = sum len[p], u <= 8).  Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_uly_unpack(const void* recv, void* y, int B, int Lmax, int Hh, int D, int u,
+                    const int* len, int slot, int nslots, int elem_bytes, xdit_stream_t stream);
+
+/* Reverse unpack: orecv[p][B][Lmax][Hh][D] (+ lrecv[p][B][Hh][Lmax]
+ * fp32, may be NULL) -> out[B][L][H][D] with h = p*Hh + hh (+ lse[B][H][L] if non-NULL).
+ * Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_uly_unpack_out(const void* orecv, const float* lrecv, int64_t peer_stride_bytes,
+                        int64_t lse_peer_stride_bytes, void* out, float* lse, int B, int L,
+                        int Lmax, int Hh, int D, int u, int elem_bytes, xdit_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* XDIT_USP_H */

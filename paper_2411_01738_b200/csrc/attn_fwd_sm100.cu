@@ -1,0 +1,391 @@
+// attn_fwd_sm100.cu -- flash-attention forward for B200 (sm_100a) on 5th-gen tensor cores.
+//
+// Computes, for one (Q block, KV block) pair of the USP ring loop:
+//     O = softmax(Q K^T / sqrt(D)) V   and   LSE = log sum_j exp(q.k_j / sqrt(D))
+// -- the "full attention" of PAPER P:257 §4.1.2 evaluated blockwise as in "a parallel version of
+// Flash Attention" (§4.1.1); readings C1 (scale 1/sqrt(D)), C2 (natural-log LSE), C3 (no mask
+// other than the ragged KV tail), C10 (bf16 inputs, fp32 scores/accumulators, P rounded RNE to
+// bf16 before P.V, O rounded RNE to bf16 on the final write).
+//
+// Design (B200-first):
+//   * one CTA = 2 query tiles of 128 rows of one (batch, head) sharing every K/V tile;
+//   * warp 8 issues TMA (128B-swizzled boxes of 128 rows x 64 columns) for Q once and for the
+//     K_j, V_j stream through a ring of smem stages (mbarrier full/empty pairs);
+//   * warp 9 (one lane) issues tcgen05.mma: S_t = Q_t K_j^T (SS, fp32 in TMEM) and
+//     O_t += P_t V_j (TS: P_t read straight from TMEM, V from smem, MN-major);
+//   * warps 0-3 / 4-7 are the softmax warpgroups of tile 0 / tile 1 (thread = query row = TMEM lane):
+//     tcgen05.ld the 128 scores, online softmax in base 2 with a lazily updated running max (O is
+//     rescaled in TMEM only when the max grows by more than 2^8), tcgen05.st of P as bf16 pairs
+//     over the consumed S columns, then the epilogue (O / l, LSE) written through an xdit_rowmap.
+//   The two tiles ping-pong: while one warpgroup runs exp2 on its S, the tensor core runs the
+//   other tile's QK^T / PV, so MUFU and tensor pipes overlap.
+// TMEM (512 columns x 128 lanes x 32 bit): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [256+D,256+2D);
+// P_t aliases the first 64 columns of S_t.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+
+#include "sm100_ptx.cuh"
+#include "xdit_internal.h"
+
+namespace xdit {
+namespace {
+
+constexpr int kBlockM = 128;      // query rows per tile (= TMEM lanes)
+constexpr int kQTiles = 2;        // query tiles per CTA
+constexpr int kBlockN = 128;      // keys per KV tile
+constexpr int kThreads = 320;     // 8 softmax warps + TMA warp + MMA warp
+constexpr int kWarpTma = 8;
+constexpr int kWarpMma = 9;
+constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only if the max grows by > 2^8
+constexpr uint32_t kTmemCols = 512;
+
+template <int D>
+struct Cfg {
+  static constexpr int kChunks = D / 64;            // 128-byte swizzle atoms along D
+  static constexpr int kChunkBytes = kBlockM * 128;  // 128 rows x 128 bytes
+  static constexpr int kTileBytes = kBlockM * D * 2;
+  static constexpr int kStages = (D == 128) ? 4 : 8;  // also forces 1 CTA/SM (TMEM is 512 cols)
+  static constexpr int kSmemQ = kQTiles * kTileBytes;
+  static constexpr int kSmemKV = kStages * kTileBytes;
+  static constexpr int kSmemBar = 256;
+  static constexpr int kSmemBytes = kSmemQ + kSmemKV + kSmemBar + 1024;
+  __host__ __device__ static constexpr uint32_t col_s(int t) { return uint32_t(t) * 128u; }
+  __host__ __device__ static constexpr uint32_t col_o(int t) { return 256u + uint32_t(t) * D; }
+};
+
+struct EpiParams {
+  void* o;
+  float* lse;
+  xdit_rowmap map;
+  int H, Sq, Skv, out_f32;
+  float scale_log2;
+};
+
+__device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
+__device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
+                          const __grid_constant__ CUtensorMap tmK,
+                          const __grid_constant__ CUtensorMap tmV, const EpiParams p) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + C::kSmemQ;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kSmemKV);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;
+  uint64_t* kv_empty = kv_full + C::kStages;
+  uint64_t* s_full = kv_empty + C::kStages;
+  uint64_t* p_full = s_full + 2;
+  uint64_t* o_full = p_full + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.y, b = blockIdx.z;
+  const int m0 = blockIdx.x * (kQTiles * kBlockM);
+  const int n_kv = (p.Skv + kBlockN - 1) / kBlockN;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&p_full[t], 4);  // one arrive per softmax warp
+      ptx::mbar_init(&o_full[t], 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == kWarpMma) {
+    ptx::tmem_alloc(tmem_slot, kTmemCols);
+    ptx::tmem_relinquish();
+  }
+  if (warp == kWarpTma && lane == 0) {
+    ptx::tma_prefetch_desc(&tmQ);
+    ptx::tma_prefetch_desc(&tmK);
+    ptx::tma_prefetch_desc(&tmV);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kWarpTma) {
+    // ===================================================== TMA producer
+    if (lane == 0) {
+      const uint64_t pol_q = ptx::policy_evict_first();
+      const uint64_t pol_kv = ptx::policy_evict_last();
+      ptx::mbar_expect_tx(q_full, kQTiles * C::kTileBytes);
+      for (int t = 0; t < kQTiles; ++t)
+        for (int c = 0; c < C::kChunks; ++c)
+          ptx::tma_load_4d(sQ + t * C::kTileBytes + c * C::kChunkBytes, &tmQ, q_full, c * 64, h,
+                           m0 + t * kBlockM, b, pol_q);
+      int it = 0;
+      for (int j = 0; j < n_kv; ++j) {
+        for (int kv = 0; kv < 2; ++kv, ++it) {
+          const int stage = it % C::kStages, round = it / C::kStages;
+          if (round > 0) ptx::mbar_wait(&kv_empty[stage], (round - 1) & 1);
+          ptx::mbar_expect_tx(&kv_full[stage], C::kTileBytes);
+          for (int c = 0; c < C::kChunks; ++c)
+            ptx::tma_load_4d(sKV + stage * C::kTileBytes + c * C::kChunkBytes, kv ? &tmV : &tmK,
+                             &kv_full[stage], c * 64, h, j * kBlockN, b, pol_kv);
+        }
+      }
+    }
+  } else if (warp == kWarpMma) {
+    // ===================================================== MMA issuer (single thread)
+    if (lane == 0) {
+      constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
+      const uint32_t sQa = ptx::smem_u32(sQ), sKVa = ptx::smem_u32(sKV);
+      // K-major operand (Q or K tile): 16-element K step k lives in atom k/4 at byte 32*(k%4).
+      auto kmaj = [&](uint32_t base, int k) -> uint64_t {
+        return ptx::sdesc_sw128(base + (k >> 2) * C::kChunkBytes + (k & 3) * 32, 16, 1024);
+      };
+      // MN-major V tile: 16-key step k starts at row 16k; 64-column atoms are kChunkBytes apart.
+      auto vdesc = [&](int stage, int k) -> uint64_t {
+        return ptx::sdesc_sw128(sKVa + stage * C::kTileBytes + k * 16 * 128, C::kChunkBytes, 1024);
+      };
+      auto kv_wait = [&](int idx) -> int {
+        const int stage = idx % C::kStages;
+        ptx::mbar_wait(&kv_full[stage], (idx / C::kStages) & 1);
+        ptx::tc_fence_after();
+        return stage;
+      };
+      auto qk = [&](int t, int sK) {
+        const uint32_t qa = sQa + t * C::kTileBytes, ka = sKVa + sK * C::kTileBytes;
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          ptx::mma_ss(tmem + C::col_s(t), kmaj(qa, k), kmaj(ka, k), idesc_qk, k > 0 ? 1u : 0u);
+      };
+      auto pv = [&](int t, int sV, bool acc) {
+#pragma unroll
+        for (int k = 0; k < kBlockN / 16; ++k)
+          ptx::mma_ts(tmem + C::col_o(t), tmem + C::col_s(t) + k * 8, vdesc(sV, k), idesc_pv,
+                      (acc || k > 0) ? 1u : 0u);
+      };
+
+      ptx::mbar_wait(q_full, 0);
+      ptx::tc_fence_after();
+      int sVprev = 0;
+      for (int j = 0; j < n_kv; ++j) {
+        const int sK = kv_wait(2 * j);
+        qk(0, sK);  // S0 = Q0 K_j^T
+        ptx::tc_commit(&s_full[0]);
+        if (j > 0) {  // O1 += P1(j-1) V_{j-1}
+          ptx::mbar_wait(&p_full[1], (j - 1) & 1);
+          ptx::tc_fence_after();
+          pv(1, sVprev, j - 1 > 0);
+          ptx::tc_commit(&kv_empty[sVprev]);
+        }
+        qk(1, sK);  // S1 = Q1 K_j^T
+        ptx::tc_commit(&s_full[1]);
+        ptx::tc_commit(&kv_empty[sK]);
+        const int sV = kv_wait(2 * j + 1);
+        ptx::mbar_wait(&p_full[0], j & 1);  // O0 += P0(j) V_j
+        ptx::tc_fence_after();
+        pv(0, sV, j > 0);
+        if (j == n_kv - 1) ptx::tc_commit(&o_full[0]);
+        sVprev = sV;
+      }
+      ptx::mbar_wait(&p_full[1], (n_kv - 1) & 1);
+      ptx::tc_fence_after();
+      pv(1, sVprev, n_kv - 1 > 0);
+      ptx::tc_commit(&o_full[1]);
+      ptx::tc_commit(&kv_empty[sVprev]);
+    }
+  } else {
+    // ===================================================== softmax warpgroups (tile t = warp/4)
+    const int t = warp >> 2, wq = warp & 3;
+    const int row_in_tile = wq * 32 + lane;
+    const uint32_t lane_off = uint32_t(wq * 32) << 16;
+    const uint32_t tS = tmem + C::col_s(t) + lane_off;
+    const uint32_t tO = tmem + C::col_o(t) + lane_off;
+    const float sl2 = p.scale_log2;
+    float m_used = 0.f, l = 0.f;
+    for (int j = 0; j < n_kv; ++j) {
+      ptx::mbar_wait(&s_full[t], j & 1);
+      ptx::tc_fence_after();
+      // pass 1: row max of the raw scores (TMEM is re-read in pass 2; keeps registers < 168)
+      const int valid = (j == n_kv - 1) ? p.Skv - j * kBlockN : kBlockN;  // ragged KV tail (C16)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; c += 2) {
+        uint32_t a[32], bq[32];
+        ptx::tmem_ld32(tS + c * 32, a);
+        ptx::tmem_ld32(tS + c * 32 + 32, bq);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (c * 32 + i < valid) mx = fmaxf(mx, u2f(a[i]));
+          if (c * 32 + 32 + i < valid) mx = fmaxf(mx, u2f(bq[i]));
+        }
+      }
+      const float m_tile = mx * sl2;
+      if (j == 0) {
+        m_used = m_tile;
+      } else {
+        const bool need = m_tile > m_used + kRescaleThresh;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = fmaxf(m_used, m_tile);
+          const float alpha = ptx::ex2(m_used - m_new);
+          l *= alpha;
+#pragma unroll
+          for (int c = 0; c < D / 32; ++c) {
+            uint32_t o[32];
+            ptx::tmem_ld32(tO + c * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+            ptx::tmem_st32(tO + c * 32, o);
+          }
+          m_used = m_new;
+        }
+      }
+      // pass 2: P = exp2(s * scale*log2e - m) -> bf16 pairs over S columns [32*half, 32*half+32)
+      const float neg_m = -m_used;
+      float rs = 0.f;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        uint32_t a[32], bq[32], pk[32];
+        ptx::tmem_ld32(tS + half * 64, a);
+        ptx::tmem_ld32(tS + half * 64 + 32, bq);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const uint32_t* src = (i < 16) ? a : bq;
+          const int e = (i & 15) * 2, col = half * 64 + (i < 16 ? 0 : 32) + e;
+          float p0 = ptx::ex2(fmaf(u2f(src[e]), sl2, neg_m));
+          float p1 = ptx::ex2(fmaf(u2f(src[e + 1]), sl2, neg_m));
+          if (col >= valid) p0 = 0.f;
+          if (col + 1 >= valid) p1 = 0.f;
+          rs += p0 + p1;
+          pk[i] = ptx::pack_bf16x2(p0, p1);
+        }
+        ptx::tmem_st32(tS + half * 32, pk);
+      }
+      l += rs;
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+    }
+    // ------------------------------------------------- epilogue: O / l, LSE
+    ptx::mbar_wait(&o_full[t], 0);
+    ptx::tc_fence_after();
+    const int row = m0 + t * kBlockM + row_in_tile;
+    const float inv_l = 1.f / l;
+    const RowDst dst = rowmap_dst(p.map, b, row, h);
+    const bool valid = row < p.Sq;
+#pragma unroll
+    for (int c = 0; c < D / 32; ++c) {
+      uint32_t o[32];
+      ptx::tmem_ld32(tO + c * 32, o);
+      ptx::tmem_ld_wait();
+      if (valid) {
+        if (p.out_f32) {
+          float4* dstp = reinterpret_cast<float4*>(static_cast<float*>(p.o) + dst.o_off + c * 32);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dstp[i] = make_float4(u2f(o[4 * i]) * inv_l, u2f(o[4 * i + 1]) * inv_l,
+                                  u2f(o[4 * i + 2]) * inv_l, u2f(o[4 * i + 3]) * inv_l);
+        } else {
+          uint4* dstp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.o) + dst.o_off + c * 32);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dstp[i] = make_uint4(ptx::pack_bf16x2(u2f(o[8 * i]) * inv_l, u2f(o[8 * i + 1]) * inv_l),
+                                 ptx::pack_bf16x2(u2f(o[8 * i + 2]) * inv_l, u2f(o[8 * i + 3]) * inv_l),
+                                 ptx::pack_bf16x2(u2f(o[8 * i + 4]) * inv_l, u2f(o[8 * i + 5]) * inv_l),
+                                 ptx::pack_bf16x2(u2f(o[8 * i + 6]) * inv_l, u2f(o[8 * i + 7]) * inv_l));
+        }
+      }
+    }
+    if (valid && p.lse) p.lse[dst.l_off] = (m_used + log2f(l)) * 0.69314718055994530942f;
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  if (warp == kWarpMma) ptx::tmem_dealloc(tmem, kTmemCols);
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult qres;
+    void* ptr = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) ==
+            cudaSuccess &&
+        qres == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+  }
+  return fn;
+}
+
+// [B][S][H][D] bf16 view with element strides (sb, ss, sh); box = 64 columns x 128 rows.
+bool make_map(CUtensorMap* map, const void* base, int B, int S, int H, int D, int64_t sb, int64_t ss,
+              int64_t sh) {
+  auto enc = get_encode_fn();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {cuuint64_t(D), cuuint64_t(H), cuuint64_t(S), cuuint64_t(B)};
+  cuuint64_t strides[3] = {cuuint64_t(sh * 2), cuuint64_t(ss * 2), cuuint64_t(sb * 2)};
+  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int D>
+cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
+  using C = Cfg<D>;
+  CUtensorMap mq, mk, mv;
+  if (!make_map(&mq, a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h) ||
+      !make_map(&mk, a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h) ||
+      !make_map(&mv, a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h))
+    return cudaErrorInvalidValue;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  EpiParams p;
+  p.o = a.o;
+  p.lse = a.lse;
+  p.map = a.omap;
+  p.H = a.H;
+  p.Sq = a.Sq;
+  p.Skv = a.Skv;
+  p.out_f32 = a.out_f32;
+  p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  dim3 grid((a.Sq + kQTiles * kBlockM - 1) / (kQTiles * kBlockM), a.H, a.B);
+  attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, st>>>(mq, mk, mv, p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st) {
+  if (a.Sq == 0 || a.B == 0) return cudaSuccess;
+  switch (a.D) {
+    case 64: return launch_d<64>(a, st);
+    case 128: return launch_d<128>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace xdit

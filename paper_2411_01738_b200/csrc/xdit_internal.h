@@ -1,0 +1,61 @@
+// xdit_internal.h -- declarations shared by the host orchestrator (xdit_usp.cpp) and the CUDA
+// kernel launchers.  Not part of the public ABI (that is include/xdit_usp.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/xdit_usp.h"
+
+namespace xdit {
+
+// Arguments of one attention launch (one Q block against one KV block).  Strides in elements.
+struct AttnArgs {
+  const void* q;
+  const void* k;
+  const void* v;
+  void* o;
+  float* lse;  // may be null
+  int B, H, Sq, Skv, D;
+  int64_t q_b, q_s, q_h;
+  int64_t kv_b, kv_s, kv_h;
+  xdit_rowmap omap;
+  int out_f32;
+};
+
+// Launchers return cudaError_t (cudaSuccess on success); argument checks happen in xdit_usp.cpp.
+cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st);  // bf16, D in {64,128}
+cudaError_t launch_attn_fwd_f32(const AttnArgs& a, cudaStream_t st);    // fp32 SIMT, D <= 256
+cudaError_t launch_lse_merge(float* o_acc, float* lse_acc, const float* o_s, const float* lse_s,
+                             int B, int S, int Hh, int D, void* fin, float* fin_lse,
+                             const xdit_rowmap* fmap, int fin_dtype, cudaStream_t st);
+cudaError_t launch_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u,
+                            int slot, int nslots, int elem_bytes, cudaStream_t st);
+cudaError_t launch_uly_unpack(const void* recv, void* y, int B, int Lmax, int Hh, int D, int u,
+                              const int* len, int slot, int nslots, int elem_bytes,
+                              cudaStream_t st);
+cudaError_t launch_uly_unpack_out(const void* orecv, const float* lrecv, int64_t peer_stride_bytes,
+                                  int64_t lse_peer_stride_bytes, void* out, float* lse, int B,
+                                  int L, int Lmax, int Hh, int D, int u, int elem_bytes,
+                                  cudaStream_t st);
+
+// Device-side row-map resolution shared by every epilogue that writes through an xdit_rowmap.
+struct RowDst {
+  int64_t o_off;  // element offset of (b, row, h, 0)
+  int64_t l_off;  // element offset of lse(b, h, row)
+};
+__host__ __device__ inline RowDst rowmap_dst(const xdit_rowmap& m, int b, int row, int h) {
+  int s = 0;
+#if defined(__CUDACC__)
+#pragma unroll
+#endif
+  for (int i = 1; i < 8; ++i)
+    if (i < m.nseg && row >= m.seg_off[i]) s = i;
+  const int64_t r = row - m.seg_off[s];
+  RowDst d;
+  d.o_off = s * m.o_seg + b * m.o_b + r * m.o_s + h * m.o_h;
+  d.l_off = s * m.l_seg + b * m.l_b + h * m.l_h + r;
+  return d;
+}
+
+}  // namespace xdit

@@ -1,0 +1,257 @@
+"""Thin ctypes binding of libxdit_usp.so (include/xdit_usp.h).
+
+Argument marshalling only: torch tensors -> device pointers, the current CUDA stream -> handle,
+status codes -> exceptions.  Every step of the hot path runs in the library's CUDA kernels and
+NCCL; there is no Python or CPU fallback -- if the extension is missing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Sequence, Tuple
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libxdit_usp.so")
+
+XDIT_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "DIVISIBILITY", 4: "COMM_MISMATCH",
+               5: "EMPTY_SHARD", 6: "ALIGNMENT", 7: "CUDA", 8: "NCCL", 9: "WORKSPACE"}
+NCCL_UNIQUE_ID_BYTES = 128
+
+
+class XditError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        self.code = code
+        self.status = XDIT_STATUS.get(code, str(code))
+        super().__init__(f"{fn} -> XDIT_ERR_{self.status} ({code}): {msg}")
+
+
+class RowMap(ctypes.Structure):
+    """xdit_rowmap: destination of an output row block (see include/xdit_usp.h)."""
+    _fields_ = [("nseg", ctypes.c_int32), ("seg_off", ctypes.c_int32 * 9),
+                ("o_seg", ctypes.c_int64), ("o_b", ctypes.c_int64), ("o_s", ctypes.c_int64),
+                ("o_h", ctypes.c_int64), ("l_seg", ctypes.c_int64), ("l_b", ctypes.c_int64),
+                ("l_h", ctypes.c_int64)]
+
+    @classmethod
+    def plain(cls, B: int, S: int, H: int, D: int) -> "RowMap":
+        """A plain [B][S][H][D] output with lse [B][H][S]."""
+        m = cls()
+        m.nseg = 1
+        m.seg_off[1] = S
+        m.o_b, m.o_s, m.o_h = S * H * D, H * D, D
+        m.l_b, m.l_h = H * S, S
+        return m
+
+
+class Plan(ctypes.Structure):
+    """xdit_plan: per-rank geometry of one USP call."""
+    _fields_ = [("nranks", ctypes.c_int32), ("rank", ctypes.c_int32), ("ulysses", ctypes.c_int32),
+                ("ring", ctypes.c_int32), ("i", ctypes.c_int32), ("j", ctypes.c_int32),
+                ("Hh", ctypes.c_int32), ("S_loc", ctypes.c_int32), ("Lmax", ctypes.c_int32),
+                ("S_blk", ctypes.c_int32), ("ring_next", ctypes.c_int32), ("ring_prev", ctypes.c_int32),
+                ("nseg", ctypes.c_int32), ("seg_off", ctypes.c_int32 * 9),
+                ("ring_src", ctypes.c_int32 * 8), ("ring_rows", ctypes.c_int32 * 8),
+                ("a2a_bytes_per_peer", ctypes.c_int64), ("ring_bytes", ctypes.c_int64 * 8)]
+
+
+_lib = None
+_vp, _i, _i64, _fp = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
+
+_SIGS = {
+    "xdit_last_error": ([], ctypes.c_char_p),
+    "xdit_version": ([], _i),
+    "xdit_usp_shard": ([_i, _i, _i, _i] + [ctypes.POINTER(_i)] * 4, _i),
+    "xdit_usp_plan": ([_i] * 8 + [ctypes.POINTER(Plan)], _i),
+    "xdit_nccl_unique_id": ([_vp], _i),
+    "xdit_comm_init": ([_vp, _i, _i, _i, _i, ctypes.POINTER(_vp)], _i),
+    "xdit_comm_create": ([_vp, _i, _i, ctypes.POINTER(_vp)], _i),
+    "xdit_comm_reserve": ([_vp, _i, _i, _i, _i, _i, _i], _i),
+    "xdit_comm_info": ([_vp] + [ctypes.POINTER(_i)] * 4, _i),
+    "xdit_comm_destroy": ([_vp], _i),
+    "xdit_usp_attention": ([_vp] * 5 + [_i] * 8 + [_vp, _vp], _i),
+    "xdit_usp_attention_f32": ([_vp] * 5 + [_i] * 8 + [_vp, _vp], _i),
+    "xdit_attn_fwd": ([_vp] * 5 + [_i] * 5 + [_i64] * 6 + [ctypes.POINTER(RowMap), _i, _i, _vp], _i),
+    "xdit_lse_merge": ([_vp] * 4 + [_i] * 4 + [_vp, _vp, ctypes.POINTER(RowMap), _i, _vp], _i),
+    "xdit_uly_pack": ([_vp, _vp] + [_i] * 10 + [_vp], _i),
+    "xdit_uly_unpack": ([_vp, _vp] + [_i] * 5 + [ctypes.POINTER(_i), _i, _i, _i, _vp], _i),
+    "xdit_uly_unpack_out": ([_vp, _vp, _i64, _i64, _vp, _vp] + [_i] * 7 + [_vp], _i),
+}
+
+
+def lib():
+    """Load libxdit_usp.so (built in-tree by paper_2411_01738_b200.build); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2411_01738_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, fn: str):
+    if rc != 0:
+        raise XditError(rc, fn, lib().xdit_last_error().decode(errors="replace"))
+
+
+def last_error() -> str:
+    return lib().xdit_last_error().decode(errors="replace")
+
+
+def version() -> int:
+    return int(lib().xdit_version())
+
+
+def exported_symbols() -> Sequence[str]:
+    return list(_SIGS)
+
+
+# ------------------------------------------------------------------------------------ host logic
+def shard(S_txt: int, S_img: int, nranks: int, g: int) -> Tuple[int, int, int, int]:
+    """(txt_off, txt_len, img_off, img_len) of SP rank g (reading C5)."""
+    v = [_i() for _ in range(4)]
+    _check(lib().xdit_usp_shard(S_txt, S_img, nranks, g, *[ctypes.byref(x) for x in v]), "xdit_usp_shard")
+    return tuple(int(x.value) for x in v)
+
+
+def plan(B: int, H: int, S_txt: int, S_img: int, D: int, ulysses: int, ring: int, rank: int) -> Plan:
+    p = Plan()
+    _check(lib().xdit_usp_plan(B, H, S_txt, S_img, D, ulysses, ring, rank, ctypes.byref(p)), "xdit_usp_plan")
+    return p
+
+
+# ------------------------------------------------------------------------------------ torch glue
+def _ptr(t) -> Optional[int]:
+    return None if t is None else t.data_ptr()
+
+
+def _stream(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+class Comm:
+    """One SP group (= one CFG group): ulysses x ring mesh, NCCL sub-communicators, workspace.
+
+    With ulysses*ring == 1 no NCCL object is created.  Otherwise rank 0 of `group` (a
+    torch.distributed process group, default WORLD) creates an NCCL unique id, which is broadcast
+    with torch.distributed; every rank then calls xdit_comm_init on its current CUDA device.
+    """
+
+    def __init__(self, ulysses: int = 1, ring: int = 1, group=None):
+        self.ulysses, self.ring = ulysses, ring
+        n = ulysses * ring
+        h = _vp()
+        if n == 1:
+            _check(lib().xdit_comm_init(None, 1, 0, 1, 1, ctypes.byref(h)), "xdit_comm_init")
+            self.rank = 0
+        else:
+            import torch
+            import torch.distributed as dist
+            rank = dist.get_rank(group)
+            if dist.get_world_size(group) != n:
+                raise XditError(4, "Comm", f"group size {dist.get_world_size(group)} != ulysses*ring={n}")
+            buf = (ctypes.c_uint8 * NCCL_UNIQUE_ID_BYTES)()
+            if rank == 0:
+                _check(lib().xdit_nccl_unique_id(ctypes.cast(buf, _vp)), "xdit_nccl_unique_id")
+            obj = [bytes(buf)]
+            src = dist.get_global_rank(group, 0) if group is not None else 0
+            dist.broadcast_object_list(obj, src=src, group=group)
+            ctypes.memmove(buf, obj[0], NCCL_UNIQUE_ID_BYTES)
+            _check(lib().xdit_comm_init(ctypes.cast(buf, _vp), n, rank, ulysses, ring, ctypes.byref(h)),
+                   "xdit_comm_init")
+            self.rank = rank
+        self.handle = h
+        self._reserved = None
+
+    def reserve(self, B: int, H: int, S_txt: int, S_img: int, D: int, elem_bytes: int = 2):
+        key = (B, H, S_txt, S_img, D, elem_bytes)
+        if self._reserved != key:
+            _check(lib().xdit_comm_reserve(self.handle, *key), "xdit_comm_reserve")
+            self._reserved = key
+        return self
+
+    def destroy(self):
+        if self.handle:
+            lib().xdit_comm_destroy(self.handle)
+            self.handle = None
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.destroy()
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def attention(q, k, v, *, S_txt: int, S_img: int, comm: Comm, ulysses: int = 1, ring: int = 1,
+              out=None, lse=None, return_lse: bool = True, stream=None):
+    """USP attention of this rank's local tokens: q, k, v [B, S_loc, H, D] (bf16 -> tcgen05 path,
+    fp32 -> SIMT fp32 path).  Returns (out, lse) with lse [B, H, S_loc] fp32 (or None)."""
+    import torch
+    B, L, H, D = q.shape
+    for t in (q, k, v):
+        if not t.is_cuda or not t.is_contiguous():
+            raise XditError(1, "attention", "q, k, v must be contiguous CUDA tensors")
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None and return_lse:
+        lse = torch.empty((B, H, L), dtype=torch.float32, device=q.device)
+    f32 = q.dtype == torch.float32
+    comm.reserve(B, H, S_txt, S_img, D, 4 if f32 else 2)
+    fn = lib().xdit_usp_attention_f32 if f32 else lib().xdit_usp_attention
+    rc = fn(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), B, H, S_txt, S_img, D, ulysses, ring,
+            _stream(stream), comm.handle)
+    _check(rc, "xdit_usp_attention_f32" if f32 else "xdit_usp_attention")
+    return out, lse
+
+
+# ------------------------------------------------------------------------------------ stage kernels
+def attn_fwd(q, k, v, o, lse, *, B: int, H: int, Sq: int, Skv: int, D: int, q_strides, kv_strides,
+             omap: RowMap, dtype: int = 0, out_f32: int = 0, stream=None):
+    """One attention launch (see xdit_attn_fwd).  Strides are (b, s, h) in elements."""
+    rc = lib().xdit_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), B, H, Sq, Skv, D,
+                             *[int(x) for x in q_strides], *[int(x) for x in kv_strides],
+                             ctypes.byref(omap), dtype, out_f32, _stream(stream))
+    _check(rc, "xdit_attn_fwd")
+
+
+def lse_merge(o_acc, lse_acc, o_s, lse_s, *, B: int, S: int, Hh: int, D: int, final=None,
+              final_lse=None, final_map: Optional[RowMap] = None, final_dtype: int = 0, stream=None):
+    rc = lib().xdit_lse_merge(_ptr(o_acc), _ptr(lse_acc), _ptr(o_s), _ptr(lse_s), B, S, Hh, D,
+                              _ptr(final), _ptr(final_lse),
+                              ctypes.byref(final_map) if final_map is not None else None,
+                              final_dtype, _stream(stream))
+    _check(rc, "xdit_lse_merge")
+
+
+def uly_pack(x, send, *, B: int, L: int, Lmax: int, H: int, D: int, u: int, slot: int, nslots: int,
+             elem_bytes: int, stream=None):
+    _check(lib().xdit_uly_pack(_ptr(x), _ptr(send), B, L, Lmax, H, D, u, slot, nslots, elem_bytes,
+                               _stream(stream)), "xdit_uly_pack")
+
+
+def uly_unpack(recv, y, *, B: int, Lmax: int, Hh: int, D: int, u: int, lens, slot: int, nslots: int,
+               elem_bytes: int, stream=None):
+    arr = (_i * 8)(*([int(x) for x in lens] + [0] * (8 - len(lens))))
+    _check(lib().xdit_uly_unpack(_ptr(recv), _ptr(y), B, Lmax, Hh, D, u, arr, slot, nslots, elem_bytes,
+                                 _stream(stream)), "xdit_uly_unpack")
+
+
+def uly_unpack_out(orecv_ptr: int, lrecv_ptr: Optional[int], peer_stride_bytes: int,
+                   lse_peer_stride_bytes: int, out, lse, *, B: int, L: int, Lmax: int, Hh: int, D: int,
+                   u: int, elem_bytes: int, stream=None):
+    _check(lib().xdit_uly_unpack_out(orecv_ptr, lrecv_ptr, peer_stride_bytes, lse_peer_stride_bytes,
+                                     _ptr(out), _ptr(lse), B, L, Lmax, Hh, D, u, elem_bytes,
+                                     _stream(stream)), "xdit_uly_unpack_out")

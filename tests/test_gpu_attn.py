@@ -1,0 +1,125 @@
+"""GPU parity of the attention kernels against the fp64 oracle.
+
+bf16 inputs -> tcgen05/TMEM/TMA kernel; fp32 inputs -> SIMT kernel.  Shapes span several 128-row
+Q and KV tiles with ragged tails, B > 1, Sq != Skv, both supported head dims, and the degenerate
+cases of the method (one key, one query, q = 0, identity attention, large magnitudes).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2411_01738_b200 import usp
+from paper_2411_01738_b200.inputs import qkv
+from tests._util import assert_bf16, assert_f32, errors, f64
+
+pytestmark = pytest.mark.gpu
+
+
+def run_attn(q, k, v, dtype=0, out_f32=0, lse=True):
+    B, Sq, H, D = q.shape
+    Skv = k.shape[1]
+    o = torch.empty(q.shape, dtype=torch.float32 if (dtype == 1 or out_f32) else torch.bfloat16, device="cuda")
+    l = torch.empty((B, H, Sq), dtype=torch.float32, device="cuda") if lse else None
+    usp.attn_fwd(q, k, v, o, l, B=B, H=H, Sq=Sq, Skv=Skv, D=D, q_strides=(Sq * H * D, H * D, D),
+                 kv_strides=(Skv * H * D, H * D, D), omap=usp.RowMap.plain(B, Sq, H, D), dtype=dtype,
+                 out_f32=out_f32)
+    torch.cuda.synchronize()
+    return o, l
+
+
+SHAPES = [  # B, H, Sq, Skv, D
+    (1, 2, 256, 256, 64),
+    (1, 2, 256, 256, 128),
+    (2, 3, 300, 333, 64),
+    (1, 2, 129, 1000, 128),
+    (1, 1, 1, 5, 64),
+    (2, 2, 513, 127, 128),
+    (1, 4, 1024, 1024, 64),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("out_f32", [0, 1])
+def test_attn_bf16_vs_oracle(shape, out_f32):
+    B, H, Sq, Skv, D = shape
+    q, _, _ = qkv(B, Sq, H, D, seed=1000 + Sq)
+    _, k, v = qkv(B, Skv, H, D, seed=2000 + Skv)
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    o, l = run_attn(q.cuda(), k.cuda(), v.cuda(), dtype=0, out_f32=out_f32)
+    assert_bf16(errors(o, l, ref_o, ref_l))
+
+
+@pytest.mark.parametrize("shape", [(1, 2, 256, 256, 64), (2, 3, 300, 333, 72), (1, 2, 129, 500, 128), (1, 1, 7, 3, 5)],
+                         ids=lambda s: "x".join(map(str, s)))
+def test_attn_f32_vs_oracle(shape):
+    B, H, Sq, Skv, D = shape
+    q, _, _ = qkv(B, Sq, H, D, seed=3000 + Sq, dtype=torch.float32)
+    _, k, v = qkv(B, Skv, H, D, seed=4000 + Skv, dtype=torch.float32)
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    o, l = run_attn(q.cuda(), k.cuda(), v.cuda(), dtype=1)
+    assert_f32(errors(o, l, ref_o, ref_l))
+
+
+def test_q_zero_gives_mean_v():
+    B, H, S, D = 1, 2, 700, 128
+    _, k, v = qkv(B, S, H, D, seed=11)
+    q = torch.zeros_like(k)
+    o, l = run_attn(q.cuda(), k.cuda(), v.cuda())
+    ref = f64(v).mean(axis=1, keepdims=True)
+    assert np.abs(f64(o) - ref).max() < 4e-3
+    assert np.abs(f64(l) - math.log(S)).max() < 1e-5
+
+
+def test_identity_attention_canary():
+    B, H, S, D, alpha = 1, 1, 1024, 64, 200.0
+    k = torch.randn(B, S, H, D, generator=torch.Generator().manual_seed(5))
+    k = k / k.norm(dim=-1, keepdim=True)
+    q = (alpha * k).to(torch.bfloat16)
+    k = k.to(torch.bfloat16)
+    v = torch.randn(B, S, H, D, generator=torch.Generator().manual_seed(6)).to(torch.bfloat16)
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    o, l = run_attn(q.cuda(), k.cuda(), v.cuda())
+    assert_bf16(errors(o, l, ref_o, ref_l))
+    assert np.abs(f64(o) - f64(v)).max() < 0.05  # O_i ~ V_i: token bookkeeping is right
+
+
+def test_two_token_D64():
+    # SURVEY §8(c) worked example at D=64: q0 = 8 ln3 e0 (rounded to bf16 8.8125), k0 = e0, k1 = 0
+    D = 64
+    q = torch.zeros(1, 2, 1, D); q[0, 0, 0, 0] = 8 * math.log(3)
+    k = torch.zeros(1, 2, 1, D); k[0, 0, 0, 0] = 1.0
+    v = torch.zeros(1, 2, 1, D); v[0, 0, 0, :] = 1.0; v[0, 1, 0, :] = 5.0
+    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
+    o, l = run_attn(q.cuda(), k.cuda(), v.cuda())
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    assert_bf16(errors(o, l, ref_o, ref_l))
+    assert abs(float(o[0, 0, 0, 0]) - 2.0) < 2e-2 and abs(float(l[0, 0, 0]) - math.log(4)) < 3e-3
+    assert abs(float(o[0, 1, 0, 0]) - 3.0) < 2e-2 and abs(float(l[0, 0, 1]) - math.log(2)) < 1e-5
+
+
+def test_large_magnitude_no_overflow():
+    B, H, S, D = 1, 2, 400, 128
+    q, k, v = qkv(B, S, H, D, seed=77, scale=30.0)
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    o, l = run_attn(q.cuda(), k.cuda(), v.cuda())
+    assert torch.isfinite(o.float()).all() and torch.isfinite(l).all()
+    e = errors(o, l, ref_o, ref_l)
+    assert e["o_maxabs"] <= 30 * 2e-2 and e["lse_maxabs"] <= 1e-2, e
+
+
+def test_determinism():
+    B, H, S, D = 1, 3, 900, 64
+    q, k, v = (t.cuda() for t in qkv(B, S, H, D, seed=5))
+    a = run_attn(q, k, v)
+    b = run_attn(q, k, v)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_unsupported_head_dim_is_rejected():
+    q = torch.zeros(1, 128, 1, 96, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(usp.XditError) as ei:
+        run_attn(q, q, q)
+    assert ei.value.status == "UNSUPPORTED"
