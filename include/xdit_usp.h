@@ -65,6 +65,10 @@ XDIT_API const char* xdit_last_error(void);
 /* Library ABI version (major*10000 + minor*100 + patch). */
 XDIT_API int xdit_version(void);
 
+/* Number of CUDA kernels this library has launched in this process (all devices, monotonic).
+ * Read before and after a region to count the library's own launches in it. */
+XDIT_API uint64_t xdit_launch_count(void);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Shard rule (§4.1.1; reading C5).  In-context conditioning: "splits both the        */
 /* Condition Tensor and Image Tensor along the sequence dimension. Then, it concatenates        */

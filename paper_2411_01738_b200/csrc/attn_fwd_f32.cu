@@ -102,7 +102,7 @@ cudaError_t launch_dq(const AttnArgs& a, cudaStream_t st) {
   dim3 grid((a.Sq + kRows - 1) / kRows, a.H, a.B);
   attn_fwd_f32_kernel<DQ><<<grid, kThreads, smem, st>>>(
       static_cast<const float*>(a.q), static_cast<const float*>(a.k),
-      static_cast<const float*>(a.v), a, float(1.0 / std::sqrt(double(a.D))));
+      static_cast<const float*>(a.v), a, float(1.0 / std::sqrt(double(a.D)))); note_launches(1);
   return cudaGetLastError();
 }
 

@@ -373,7 +373,7 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.out_f32 = a.out_f32;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
   dim3 grid((a.Sq + kQTiles * kBlockM - 1) / (kQTiles * kBlockM), a.H, a.B);
-  attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, st>>>(mq, mk, mv, p);
+  attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, st>>>(mq, mk, mv, p); note_launches(1);
   return cudaGetLastError();
 }
 

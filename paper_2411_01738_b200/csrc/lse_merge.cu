@@ -78,7 +78,7 @@ cudaError_t launch_lse_merge(float* o_acc, float* lse_acc, const float* o_s, con
   xdit_rowmap m{};
   if (fmap) m = *fmap;
   lse_merge_kernel<<<unsigned(blocks), kWarps * 32, 0, st>>>(o_acc, lse_acc, o_s, lse_s, B, S, Hh, D, fin,
-                                                             fin_lse, m, fin_dtype);
+                                                             fin_lse, m, fin_dtype); note_launches(1);
   return cudaGetLastError();
 }
 

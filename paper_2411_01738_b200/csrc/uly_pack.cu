@@ -118,10 +118,10 @@ cudaError_t launch_uly_pack(const void* x, void* send, int B, int L, int Lmax, i
   if (n == 0) return cudaSuccess;
   const unsigned g = grid_for(n, 256);
   switch (vb) {
-    case 16: pack_kernel<uint4><<<g, 256, 0, st>>>((const uint4*)x, (uint4*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
-    case 8: pack_kernel<uint2><<<g, 256, 0, st>>>((const uint2*)x, (uint2*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
-    case 4: pack_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)x, (uint32_t*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
-    default: pack_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)x, (uint16_t*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
+    case 16: pack_kernel<uint4><<<g, 256, 0, st>>>((const uint4*)x, (uint4*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
+    case 8: pack_kernel<uint2><<<g, 256, 0, st>>>((const uint2*)x, (uint2*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
+    case 4: pack_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)x, (uint32_t*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
+    default: pack_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)x, (uint16_t*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
   }
   return cudaGetLastError();
 }
@@ -140,10 +140,10 @@ cudaError_t launch_uly_unpack(const void* recv, void* y, int B, int Lmax, int Hh
   if (n == 0) return cudaSuccess;
   const unsigned g = grid_for(n, 256);
   switch (vb) {
-    case 16: unpack_kernel<uint4><<<g, 256, 0, st>>>((const uint4*)recv, (uint4*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); break;
-    case 8: unpack_kernel<uint2><<<g, 256, 0, st>>>((const uint2*)recv, (uint2*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); break;
-    case 4: unpack_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)recv, (uint32_t*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); break;
-    default: unpack_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)recv, (uint16_t*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); break;
+    case 16: unpack_kernel<uint4><<<g, 256, 0, st>>>((const uint4*)recv, (uint4*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); note_launches(1); break;
+    case 8: unpack_kernel<uint2><<<g, 256, 0, st>>>((const uint2*)recv, (uint2*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); note_launches(1); break;
+    case 4: unpack_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)recv, (uint32_t*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); note_launches(1); break;
+    default: unpack_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)recv, (uint16_t*)y, B, Lmax, Hh, vpr, u, lo, hi, S_blk, slot, nslots); note_launches(1); break;
   }
   return cudaGetLastError();
 }
@@ -158,17 +158,17 @@ cudaError_t launch_uly_unpack_out(const void* orecv, const float* lrecv, int64_t
     const unsigned g = grid_for(n, 256);
     const char* src = static_cast<const char*>(orecv);
     switch (vb) {
-      case 16: unpack_out_kernel<uint4><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint4*)out, B, L, Lmax, Hh, H, vpr); break;
-      case 8: unpack_out_kernel<uint2><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint2*)out, B, L, Lmax, Hh, H, vpr); break;
-      case 4: unpack_out_kernel<uint32_t><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint32_t*)out, B, L, Lmax, Hh, H, vpr); break;
-      default: unpack_out_kernel<uint16_t><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint16_t*)out, B, L, Lmax, Hh, H, vpr); break;
+      case 16: unpack_out_kernel<uint4><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint4*)out, B, L, Lmax, Hh, H, vpr); note_launches(1); break;
+      case 8: unpack_out_kernel<uint2><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint2*)out, B, L, Lmax, Hh, H, vpr); note_launches(1); break;
+      case 4: unpack_out_kernel<uint32_t><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint32_t*)out, B, L, Lmax, Hh, H, vpr); note_launches(1); break;
+      default: unpack_out_kernel<uint16_t><<<g, 256, 0, st>>>(src, peer_stride_bytes, (uint16_t*)out, B, L, Lmax, Hh, H, vpr); note_launches(1); break;
     }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
   if (lse && lrecv && int64_t(B) * H * L > 0) {
     unpack_lse_kernel<<<grid_for(int64_t(B) * H * L, 256), 256, 0, st>>>(
-        reinterpret_cast<const char*>(lrecv), lse_peer_stride_bytes, lse, B, L, Lmax, Hh, H);
+        reinterpret_cast<const char*>(lrecv), lse_peer_stride_bytes, lse, B, L, Lmax, Hh, H); note_launches(1);
   }
   return cudaGetLastError();
 }

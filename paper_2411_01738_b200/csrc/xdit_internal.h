@@ -9,6 +9,9 @@
 
 namespace xdit {
 
+// Count one kernel launch of this library (xdit_launch_count()).
+void note_launches(int n);
+
 // Arguments of one attention launch (one Q block against one KV block).  Strides in elements.
 struct AttnArgs {
   const void* q;

@@ -10,6 +10,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -19,6 +20,11 @@
 #include "xdit_internal.h"
 
 using xdit::AttnArgs;
+
+namespace xdit {
+static std::atomic<unsigned long long> g_launches{0};
+void note_launches(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
+}  // namespace xdit
 
 namespace {
 
@@ -420,6 +426,8 @@ extern "C" {
 const char* xdit_last_error(void) { return g_err.c_str(); }
 
 int xdit_version(void) { return 100; }
+
+uint64_t xdit_launch_count(void) { return xdit::g_launches.load(std::memory_order_relaxed); }
 
 int xdit_usp_shard(int S_txt, int S_img, int nranks, int g, int* txt_off, int* txt_len,
                    int* img_off, int* img_len) {

@@ -60,6 +60,7 @@ _vp, _i, _i64, _fp = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_voi
 _SIGS = {
     "xdit_last_error": ([], ctypes.c_char_p),
     "xdit_version": ([], _i),
+    "xdit_launch_count": ([], ctypes.c_uint64),
     "xdit_usp_shard": ([_i, _i, _i, _i] + [ctypes.POINTER(_i)] * 4, _i),
     "xdit_usp_plan": ([_i] * 8 + [ctypes.POINTER(Plan)], _i),
     "xdit_nccl_unique_id": ([_vp], _i),
@@ -68,11 +69,11 @@ _SIGS = {
     "xdit_comm_reserve": ([_vp, _i, _i, _i, _i, _i, _i], _i),
     "xdit_comm_info": ([_vp] + [ctypes.POINTER(_i)] * 4, _i),
     "xdit_comm_destroy": ([_vp], _i),
-    "xdit_usp_attention": ([_vp] * 5 + [_i] * 8 + [_vp, _vp], _i),
-    "xdit_usp_attention_f32": ([_vp] * 5 + [_i] * 8 + [_vp, _vp], _i),
+    "xdit_usp_attention": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
+    "xdit_usp_attention_f32": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
     "xdit_attn_fwd": ([_vp] * 5 + [_i] * 5 + [_i64] * 6 + [ctypes.POINTER(RowMap), _i, _i, _vp], _i),
     "xdit_lse_merge": ([_vp] * 4 + [_i] * 4 + [_vp, _vp, ctypes.POINTER(RowMap), _i, _vp], _i),
-    "xdit_uly_pack": ([_vp, _vp] + [_i] * 10 + [_vp], _i),
+    "xdit_uly_pack": ([_vp, _vp] + [_i] * 9 + [_vp], _i),
     "xdit_uly_unpack": ([_vp, _vp] + [_i] * 5 + [ctypes.POINTER(_i), _i, _i, _i, _vp], _i),
     "xdit_uly_unpack_out": ([_vp, _vp, _i64, _i64, _vp, _vp] + [_i] * 7 + [_vp], _i),
 }
@@ -105,6 +106,11 @@ def last_error() -> str:
 
 def version() -> int:
     return int(lib().xdit_version())
+
+
+def launch_count() -> int:
+    """Kernels this library has launched in this process (xdit_launch_count)."""
+    return int(lib().xdit_launch_count())
 
 
 def exported_symbols() -> Sequence[str]:
