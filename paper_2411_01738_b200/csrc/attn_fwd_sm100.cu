@@ -68,6 +68,97 @@ struct EpiParams {
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
 
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void up2(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
+// Pass 1 of the softmax of one 128-key tile: the row max of the raw scores S[row, 0:128) read from
+// TMEM (this thread's lane).  MASK: keys >= valid are excluded (ragged KV tail).  Four independent
+// FMNMX3 chains keep the dependency depth at 16.
+template <bool MASK>
+__device__ __forceinline__ float row_max(uint32_t tS, int valid) {
+  float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < 4; c += 2) {
+    uint32_t a[32], bq[32];
+    ptx::tmem_ld32(tS + c * 32, a);
+    ptx::tmem_ld32(tS + c * 32 + 32, bq);
+    ptx::tmem_ld_wait();
+    if (MASK) {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        if (c * 32 + i >= valid) a[i] = f2u(-INFINITY);
+        if (c * 32 + 32 + i >= valid) bq[i] = f2u(-INFINITY);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      m0 = fmax3(m0, u2f(a[i]), u2f(a[i + 1]));
+      m1 = fmax3(m1, u2f(a[i + 2]), u2f(a[i + 3]));
+      m2 = fmax3(m2, u2f(bq[i]), u2f(bq[i + 1]));
+      m3 = fmax3(m3, u2f(bq[i + 2]), u2f(bq[i + 3]));
+    }
+  }
+  return fmax3(m0, m1, fmaxf(m2, m3));
+}
+
+// Pass 2: P = exp2(S * scale*log2e - m) for the tile, written back to TMEM as bf16 pairs over the
+// first 64 columns of S (the A operand of the P.V MMA).  Returns the fp32 row sum of P.
+// FFMA2 / FADD2 process two columns per instruction; MUFU.EX2 does the exponentials.
+template <bool MASK>
+__device__ __forceinline__ float exp_store_p(uint32_t tS, int valid, float sl2, float neg_m) {
+  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(neg_m, neg_m);
+  uint64_t acc0 = pk2(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint32_t a[32], bq[32], pk[32];
+    ptx::tmem_ld32(tS + half * 64, a);
+    ptx::tmem_ld32(tS + half * 64 + 32, bq);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t* src = (i < 16) ? a : bq;
+      const int e = (i & 15) * 2, col = half * 64 + (i < 16 ? 0 : 32) + e;
+      const uint64_t x = fma2(pk2(u2f(src[e]), u2f(src[e + 1])), sc2, nm2);
+      float x0, x1;
+      up2(x, x0, x1);
+      float p0 = ptx::ex2(x0), p1 = ptx::ex2(x1);
+      if (MASK) {
+        if (col >= valid) p0 = 0.f;
+        if (col + 1 >= valid) p1 = 0.f;
+      }
+      if (i & 1) acc1 = add2(acc1, pk2(p0, p1));
+      else acc0 = add2(acc0, pk2(p0, p1));
+      pk[i] = ptx::pack_bf16x2(p0, p1);
+    }
+    ptx::tmem_st32(tS + half * 32, pk);
+  }
+  float s0, s1, s2, s3;
+  up2(acc0, s0, s1);
+  up2(acc1, s2, s3);
+  return (s0 + s1) + (s2 + s3);
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -216,21 +307,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < n_kv; ++j) {
       ptx::mbar_wait(&s_full[t], j & 1);
       ptx::tc_fence_after();
-      // pass 1: row max of the raw scores (TMEM is re-read in pass 2; keeps registers < 168)
-      const int valid = (j == n_kv - 1) ? p.Skv - j * kBlockN : kBlockN;  // ragged KV tail (C16)
-      float mx = -INFINITY;
-#pragma unroll
-      for (int c = 0; c < 4; c += 2) {
-        uint32_t a[32], bq[32];
-        ptx::tmem_ld32(tS + c * 32, a);
-        ptx::tmem_ld32(tS + c * 32 + 32, bq);
-        ptx::tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          if (c * 32 + i < valid) mx = fmaxf(mx, u2f(a[i]));
-          if (c * 32 + 32 + i < valid) mx = fmaxf(mx, u2f(bq[i]));
-        }
-      }
+      const bool ragged = (j == n_kv - 1) && (p.Skv - j * kBlockN < kBlockN);
+      const int valid = p.Skv - j * kBlockN;  // ragged KV tail (reading C16)
+      const float mx = ragged ? row_max<true>(tS, valid) : row_max<false>(tS, valid);
       const float m_tile = mx * sl2;
       if (j == 0) {
         m_used = m_tile;
@@ -252,28 +331,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_used = m_new;
         }
       }
-      // pass 2: P = exp2(s * scale*log2e - m) -> bf16 pairs over S columns [32*half, 32*half+32)
-      const float neg_m = -m_used;
-      float rs = 0.f;
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {
-        uint32_t a[32], bq[32], pk[32];
-        ptx::tmem_ld32(tS + half * 64, a);
-        ptx::tmem_ld32(tS + half * 64 + 32, bq);
-        ptx::tmem_ld_wait();
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const uint32_t* src = (i < 16) ? a : bq;
-          const int e = (i & 15) * 2, col = half * 64 + (i < 16 ? 0 : 32) + e;
-          float p0 = ptx::ex2(fmaf(u2f(src[e]), sl2, neg_m));
-          float p1 = ptx::ex2(fmaf(u2f(src[e + 1]), sl2, neg_m));
-          if (col >= valid) p0 = 0.f;
-          if (col + 1 >= valid) p1 = 0.f;
-          rs += p0 + p1;
-          pk[i] = ptx::pack_bf16x2(p0, p1);
-        }
-        ptx::tmem_st32(tS + half * 32, pk);
-      }
+      const float rs = ragged ? exp_store_p<true>(tS, valid, sl2, -m_used)
+                              : exp_store_p<false>(tS, valid, sl2, -m_used);
       l += rs;
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
