@@ -53,7 +53,7 @@ __global__ void unpack_kernel(const V* __restrict__ recv, V* __restrict__ y, int
     int p = 0, off = 0;
 #pragma unroll
     for (int q = 0; q < 7; ++q)
-      if (q + 1 < u && t >= off + len[q]) {
+      if (q + 1 < u && p == q && t >= off + len[q]) {  // segments are consecutive
         off += len[q];
         p = q + 1;
       }

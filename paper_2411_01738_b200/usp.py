@@ -133,7 +133,10 @@ def plan(B: int, H: int, S_txt: int, S_img: int, D: int, ulysses: int, ring: int
 
 # ------------------------------------------------------------------------------------ torch glue
 def _ptr(t) -> Optional[int]:
-    return None if t is None else t.data_ptr()
+    """Device pointer of a tensor (or a raw integer address, passed through)."""
+    if t is None or isinstance(t, int):
+        return t
+    return t.data_ptr()
 
 
 def _stream(stream=None) -> int:
