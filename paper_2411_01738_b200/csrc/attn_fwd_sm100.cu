@@ -27,6 +27,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 
 #include "sm100_ptx.cuh"
 #include "xdit_internal.h"
@@ -42,6 +43,7 @@ constexpr int kWarpTma = 8;
 constexpr int kWarpMma = 9;
 constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only if the max grows by > 2^8
 constexpr uint32_t kTmemCols = 512;
+constexpr int kDefaultEmu = 3;  // exp2 pairs (of every 8) evaluated by polynomial on the FMA pipe
 
 template <int D>
 struct Cfg {
@@ -63,6 +65,7 @@ struct EpiParams {
   xdit_rowmap map;
   int H, Sq, Skv, out_f32;
   float scale_log2;
+  int diag;  // profiling only (XDIT_DIAG): 1 = softmax does no math, 2 = also no MMA<-softmax wait
 };
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
@@ -122,10 +125,38 @@ __device__ __forceinline__ float row_max(uint32_t tS, int valid) {
   return fmax3(m0, m1, fmaxf(m2, m3));
 }
 
+// exp2 of two packed fp32 values on the FMA pipe (no MUFU): Cody-Waite split x = j + f with
+// j = round(x) (magic-number add), f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (Chebyshev fit on
+// [-0.5, 0.5], max relative error 1.0e-4 -- below the bf16 rounding P gets anyway); 2^j is added
+// straight into the exponent field.  x is clamped at -125 so the result stays a normal number.
+__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
+  float x0, x1;
+  up2(x2, x0, x1);
+  x0 = fmaxf(x0, -125.f);
+  x1 = fmaxf(x1, -125.f);
+  const uint64_t xc = pk2(x0, x1);
+  const uint64_t magic = pk2(12582912.f, 12582912.f), nmagic = pk2(-12582912.f, -12582912.f);
+  const uint64_t t = add2(xc, magic);             // 1.5*2^23 + round(x)
+  const uint64_t j = add2(t, nmagic);             // round(x)
+  const uint64_t f = fma2(j, pk2(-1.f, -1.f), xc);  // x - round(x)
+  uint64_t pp = fma2(f, pk2(0.055922120809555054f, 0.055922120809555054f),
+                     pk2(0.2426406890153885f, 0.2426406890153885f));
+  pp = fma2(f, pp, pk2(0.6931210160255432f, 0.6931210160255432f));
+  pp = fma2(f, pp, pk2(0.9999244213104248f, 0.9999244213104248f));
+  float p0, p1, t0, t1;
+  up2(pp, p0, p1);
+  up2(t, t0, t1);
+  // (bits(t) << 23) == round(x) << 23 (mod 2^32): the magic's own bits shift out
+  const int r0 = __float_as_int(t0) * (1 << 23) + __float_as_int(p0);
+  const int r1 = __float_as_int(t1) * (1 << 23) + __float_as_int(p1);
+  return pk2(__int_as_float(r0), __int_as_float(r1));
+}
+
 // Pass 2: P = exp2(S * scale*log2e - m) for the tile, written back to TMEM as bf16 pairs over the
 // first 64 columns of S (the A operand of the P.V MMA).  Returns the fp32 row sum of P.
-// FFMA2 / FADD2 process two columns per instruction; MUFU.EX2 does the exponentials.
-template <bool MASK>
+// FFMA2 / FADD2 process two columns per instruction; MUFU.EX2 does the exponentials except for EMU
+// of every 8 column pairs, which use exp2_poly2 on the FMA pipe so MUFU stops being the co-bottleneck.
+template <bool MASK, int EMU>
 __device__ __forceinline__ float exp_store_p(uint32_t tS, int valid, float sl2, float neg_m) {
   const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(neg_m, neg_m);
   uint64_t acc0 = pk2(0.f, 0.f), acc1 = acc0;
@@ -140,9 +171,15 @@ __device__ __forceinline__ float exp_store_p(uint32_t tS, int valid, float sl2, 
       const uint32_t* src = (i < 16) ? a : bq;
       const int e = (i & 15) * 2, col = half * 64 + (i < 16 ? 0 : 32) + e;
       const uint64_t x = fma2(pk2(u2f(src[e]), u2f(src[e + 1])), sc2, nm2);
-      float x0, x1;
-      up2(x, x0, x1);
-      float p0 = ptx::ex2(x0), p1 = ptx::ex2(x1);
+      float p0, p1;
+      if ((i & 7) < EMU) {
+        up2(exp2_poly2(x), p0, p1);
+      } else {
+        float x0, x1;
+        up2(x, x0, x1);
+        p0 = ptx::ex2(x0);
+        p1 = ptx::ex2(x1);
+      }
       if (MASK) {
         if (col >= valid) p0 = 0.f;
         if (col + 1 >= valid) p1 = 0.f;
@@ -159,7 +196,7 @@ __device__ __forceinline__ float exp_store_p(uint32_t tS, int valid, float sl2, 
   return (s0 + s1) + (s2 + s3);
 }
 
-template <int D>
+template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
@@ -274,7 +311,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         qk(0, sK);  // S0 = Q0 K_j^T
         ptx::tc_commit(&s_full[0]);
         if (j > 0) {  // O1 += P1(j-1) V_{j-1}
-          ptx::mbar_wait(&p_full[1], (j - 1) & 1);
+          if (p.diag < 2) ptx::mbar_wait(&p_full[1], (j - 1) & 1);
           ptx::tc_fence_after();
           pv(1, sVprev, j - 1 > 0);
           ptx::tc_commit(&kv_empty[sVprev]);
@@ -283,13 +320,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_commit(&s_full[1]);
         ptx::tc_commit(&kv_empty[sK]);
         const int sV = kv_wait(2 * j + 1);
-        ptx::mbar_wait(&p_full[0], j & 1);  // O0 += P0(j) V_j
+        if (p.diag < 2) ptx::mbar_wait(&p_full[0], j & 1);  // O0 += P0(j) V_j
         ptx::tc_fence_after();
         pv(0, sV, j > 0);
         if (j == n_kv - 1) ptx::tc_commit(&o_full[0]);
         sVprev = sV;
       }
-      ptx::mbar_wait(&p_full[1], (n_kv - 1) & 1);
+      if (p.diag < 2) ptx::mbar_wait(&p_full[1], (n_kv - 1) & 1);
       ptx::tc_fence_after();
       pv(1, sVprev, n_kv - 1 > 0);
       ptx::tc_commit(&o_full[1]);
@@ -307,6 +344,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int j = 0; j < n_kv; ++j) {
       ptx::mbar_wait(&s_full[t], j & 1);
       ptx::tc_fence_after();
+      if (p.diag) {  // profiling: measure the MMA/TMA skeleton without the softmax
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+        continue;
+      }
       const bool ragged = (j == n_kv - 1) && (p.Skv - j * kBlockN < kBlockN);
       const int valid = p.Skv - j * kBlockN;  // ragged KV tail (reading C16)
       const float mx = ragged ? row_max<true>(tS, valid) : row_max<false>(tS, valid);
@@ -331,8 +373,8 @@ __global__ void __launch_bounds__(kThreads, 1)
           m_used = m_new;
         }
       }
-      const float rs = ragged ? exp_store_p<true>(tS, valid, sl2, -m_used)
-                              : exp_store_p<false>(tS, valid, sl2, -m_used);
+      const float rs = ragged ? exp_store_p<true, 0>(tS, valid, sl2, -m_used)
+                              : exp_store_p<false, EMU>(tS, valid, sl2, -m_used);
       l += rs;
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
@@ -407,6 +449,21 @@ bool make_map(CUtensorMap* map, const void* base, int B, int S, int H, int D, in
   return r == CUDA_SUCCESS;
 }
 
+template <int D, int EMU>
+cudaError_t launch_kernel(dim3 grid, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
+                          const EpiParams& p, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, EMU>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<D>::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  attn_fwd_sm100_kernel<D, EMU><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(mq, mk, mv, p);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
 template <int D>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   using C = Cfg<D>;
@@ -415,13 +472,6 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
       !make_map(&mk, a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h) ||
       !make_map(&mv, a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h))
     return cudaErrorInvalidValue;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmemBytes);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
   EpiParams p;
   p.o = a.o;
   p.lse = a.lse;
@@ -431,9 +481,23 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.Skv = a.Skv;
   p.out_f32 = a.out_f32;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  static const int diag = [] {
+    const char* e = std::getenv("XDIT_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.diag = diag;
   dim3 grid((a.Sq + kQTiles * kBlockM - 1) / (kQTiles * kBlockM), a.H, a.B);
-  attn_fwd_sm100_kernel<D><<<grid, kThreads, C::kSmemBytes, st>>>(mq, mk, mv, p); note_launches(1);
-  return cudaGetLastError();
+  // fraction of exp2 moved to the FMA pipe: EMU of every 8 column pairs (XDIT_EXP_EMU overrides)
+  static const int emu = [] {
+    const char* e = std::getenv("XDIT_EXP_EMU");
+    return e ? std::atoi(e) : kDefaultEmu;
+  }();
+  switch (emu) {
+    case 0: return launch_kernel<D, 0>(grid, mq, mk, mv, p, st);
+    case 2: return launch_kernel<D, 2>(grid, mq, mk, mv, p, st);
+    case 4: return launch_kernel<D, 4>(grid, mq, mk, mv, p, st);
+    default: return launch_kernel<D, 3>(grid, mq, mk, mv, p, st);
+  }
 }
 
 }  // namespace
