@@ -148,7 +148,7 @@ XDIT_API int xdit_usp_plan(int B, int H, int S_txt, int S_img, int D, int ulysse
 /* q, k, v, out : this rank's local tokens, [B][S_loc][H][D] contiguous, bf16; S_loc from        */
 /*                xdit_usp_shard(S_txt, S_img, ulysses*ring, rank).  16-byte aligned.            */
 /* lse          : fp32 [B][H][S_loc] (natural log) or NULL to skip (reading C15).               */
-/* B, H, D      : batch of this SP (CFG) group, heads, head dim.  D in {64, 128} (UNSUPPORTED    */
+/* B, H, D      : batch of this SP (CFG) group, heads, head dim.  D in {64, 72, 128} (UNSUPPORTED*/
 /*                otherwise; the fp32 entry point takes any D in [1, 256]).                     */
 /* S_txt, S_img : GLOBAL text / image token counts of the joint sequence.                       */
 /* ulysses,ring : degrees; must equal the handle's; H % ulysses == 0 (DIVISIBILITY).             */
@@ -195,7 +195,7 @@ typedef struct xdit_rowmap {
 /* Flash attention forward of one (Q block, KV block) pair -- SURVEY §8(a) step a6.
  * q: [B][Sq][H][D] with strides (q_b, q_s, q_h); k, v: [B][Skv][H][D] with strides
  * (kv_b, kv_s, kv_h) shared by k and v.  dtype: 0 = bf16 inputs on the tcgen05/TMEM/TMA kernel
- * (D in {64,128}; q,k,v 16-byte aligned, strides multiples of 8 elements), 1 = fp32 inputs on the
+ * (D in {64,72,128}; q,k,v 16-byte aligned, strides multiples of 8 elements), 1 = fp32 inputs on the
  * SIMT kernel (D in [1,256]).  out_f32: 0 writes O as bf16 through `omap` (final output);
  * 1 writes O as fp32 through `omap` (ring partial).  lse may be NULL (skipped).
  * Errors: INVALID_ARG, UNSUPPORTED, ALIGNMENT, CUDA. */

@@ -47,16 +47,23 @@ constexpr int kDefaultEmu = 3;  // exp2 pairs (of every 8) evaluated by polynomi
 
 template <int D>
 struct Cfg {
-  static constexpr int kChunks = D / 64;            // 128-byte swizzle atoms along D
-  static constexpr int kChunkBytes = kBlockM * 128;  // 128 rows x 128 bytes
-  static constexpr int kTileBytes = kBlockM * D * 2;
+  // Head dim layout in smem: D/64 atoms of 64 columns, 128-byte swizzle; D = 72 adds one atom of 16
+  // columns with 32-byte swizzle whose last 8 columns TMA zero-fills (K padded to the MMA K step 16).
+  static constexpr int kN128 = D / 64;
+  static constexpr bool kTail16 = (D % 64) != 0;
+  static constexpr int kDp = kN128 * 64 + (kTail16 ? 16 : 0);  // padded head dim (MMA K / PV N)
+  static constexpr int kAtom128 = kBlockM * 128;  // 128 rows x 128 B
+  static constexpr int kAtom32 = kBlockM * 32;    // 128 rows x 32 B
+  static constexpr int kTileBytes = kN128 * kAtom128 + (kTail16 ? kAtom32 : 0);
   static constexpr int kStages = (D == 128) ? 4 : 8;  // also forces 1 CTA/SM (TMEM is 512 cols)
   static constexpr int kSmemQ = kQTiles * kTileBytes;
   static constexpr int kSmemKV = kStages * kTileBytes;
   static constexpr int kSmemBar = 256;
   static constexpr int kSmemBytes = kSmemQ + kSmemKV + kSmemBar + 1024;
+  static_assert(D == 64 || D == 72 || D == 128, "head dim");
+  static_assert(kTileBytes % 1024 == 0, "tiles must keep 1024-byte alignment for the swizzle");
   __host__ __device__ static constexpr uint32_t col_s(int t) { return uint32_t(t) * 128u; }
-  __host__ __device__ static constexpr uint32_t col_o(int t) { return 256u + uint32_t(t) * D; }
+  __host__ __device__ static constexpr uint32_t col_o(int t) { return 256u + uint32_t(t) * kDp; }
 };
 
 struct EpiParams {
@@ -126,9 +133,10 @@ __device__ __forceinline__ float row_max(uint32_t tS, int valid) {
 }
 
 // exp2 of two packed fp32 values on the FMA pipe (no MUFU): Cody-Waite split x = j + f with
-// j = round(x) (magic-number add), f in [-0.5, 0.5]; 2^f by a degree-3 polynomial (Chebyshev fit on
-// [-0.5, 0.5], max relative error 1.0e-4 -- below the bf16 rounding P gets anyway); 2^j is added
-// straight into the exponent field.  x is clamped at -125 so the result stays a normal number.
+// j = round(x) (magic-number add), f in [-0.5, 0.5]; 2^f by a degree-4 polynomial with p(0) = 1
+// exactly (minimax on [-0.5, 0.5], max relative error 2.9e-6, mean 3e-7 -- far below the bf16
+// rounding P gets anyway, and no bias on the row sum l); 2^j is added straight into the exponent
+// field.  x is clamped at -125 so the result stays a normal number.
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
   float x0, x1;
   up2(x2, x0, x1);
@@ -139,10 +147,11 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
   const uint64_t t = add2(xc, magic);             // 1.5*2^23 + round(x)
   const uint64_t j = add2(t, nmagic);             // round(x)
   const uint64_t f = fma2(j, pk2(-1.f, -1.f), xc);  // x - round(x)
-  uint64_t pp = fma2(f, pk2(0.055922120809555054f, 0.055922120809555054f),
-                     pk2(0.2426406890153885f, 0.2426406890153885f));
-  pp = fma2(f, pp, pk2(0.6931210160255432f, 0.6931210160255432f));
-  pp = fma2(f, pp, pk2(0.9999244213104248f, 0.9999244213104248f));
+  uint64_t pp = fma2(f, pk2(0.009582849219441414f, 0.009582849219441414f),
+                     pk2(0.055906426161527634f, 0.055906426161527634f));
+  pp = fma2(f, pp, pk2(0.24024099111557007f, 0.24024099111557007f));
+  pp = fma2(f, pp, pk2(0.6931241750717163f, 0.6931241750717163f));
+  pp = fma2(f, pp, pk2(1.f, 1.f));
   float p0, p1, t0, t1;
   up2(pp, p0, p1);
   up2(t, t0, t1);
@@ -200,7 +209,10 @@ template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
                           const __grid_constant__ CUtensorMap tmK,
-                          const __grid_constant__ CUtensorMap tmV, const EpiParams p) {
+                          const __grid_constant__ CUtensorMap tmV,
+                          const __grid_constant__ CUtensorMap tmQ16,
+                          const __grid_constant__ CUtensorMap tmK16,
+                          const __grid_constant__ CUtensorMap tmV16, const EpiParams p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -242,6 +254,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tma_prefetch_desc(&tmQ);
     ptx::tma_prefetch_desc(&tmK);
     ptx::tma_prefetch_desc(&tmV);
+    if (C::kTail16) {
+      ptx::tma_prefetch_desc(&tmQ16);
+      ptx::tma_prefetch_desc(&tmK16);
+      ptx::tma_prefetch_desc(&tmV16);
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -254,19 +271,27 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint64_t pol_q = ptx::policy_evict_first();
       const uint64_t pol_kv = ptx::policy_evict_last();
       ptx::mbar_expect_tx(q_full, kQTiles * C::kTileBytes);
-      for (int t = 0; t < kQTiles; ++t)
-        for (int c = 0; c < C::kChunks; ++c)
-          ptx::tma_load_4d(sQ + t * C::kTileBytes + c * C::kChunkBytes, &tmQ, q_full, c * 64, h,
+      for (int t = 0; t < kQTiles; ++t) {
+        for (int c = 0; c < C::kN128; ++c)
+          ptx::tma_load_4d(sQ + t * C::kTileBytes + c * C::kAtom128, &tmQ, q_full, c * 64, h,
                            m0 + t * kBlockM, b, pol_q);
+        if (C::kTail16)
+          ptx::tma_load_4d(sQ + t * C::kTileBytes + C::kN128 * C::kAtom128, &tmQ16, q_full,
+                           C::kN128 * 64, h, m0 + t * kBlockM, b, pol_q);
+      }
       int it = 0;
       for (int j = 0; j < n_kv; ++j) {
         for (int kv = 0; kv < 2; ++kv, ++it) {
           const int stage = it % C::kStages, round = it / C::kStages;
           if (round > 0) ptx::mbar_wait(&kv_empty[stage], (round - 1) & 1);
           ptx::mbar_expect_tx(&kv_full[stage], C::kTileBytes);
-          for (int c = 0; c < C::kChunks; ++c)
-            ptx::tma_load_4d(sKV + stage * C::kTileBytes + c * C::kChunkBytes, kv ? &tmV : &tmK,
+          for (int c = 0; c < C::kN128; ++c)
+            ptx::tma_load_4d(sKV + stage * C::kTileBytes + c * C::kAtom128, kv ? &tmV : &tmK,
                              &kv_full[stage], c * 64, h, j * kBlockN, b, pol_kv);
+          if (C::kTail16)
+            ptx::tma_load_4d(sKV + stage * C::kTileBytes + C::kN128 * C::kAtom128,
+                             kv ? &tmV16 : &tmK16, &kv_full[stage], C::kN128 * 64, h, j * kBlockN,
+                             b, pol_kv);
         }
       }
     }
@@ -274,15 +299,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ===================================================== MMA issuer (single thread)
     if (lane == 0) {
       constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBlockM, D, 0, 1);
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBlockM, C::kTail16 ? 64 : D, 0, 1);
+      constexpr uint32_t idesc_pv16 = ptx::idesc_bf16_f32(kBlockM, 16, 0, 1);
       const uint32_t sQa = ptx::smem_u32(sQ), sKVa = ptx::smem_u32(sKV);
-      // K-major operand (Q or K tile): 16-element K step k lives in atom k/4 at byte 32*(k%4).
+      // K-major operand (Q or K tile): 16-element K step k lives in 128B atom k/4 at byte 32*(k%4);
+      // the D=72 tail step is the whole 32-byte row of the 32B-swizzled atom.
       auto kmaj = [&](uint32_t base, int k) -> uint64_t {
-        return ptx::sdesc_sw128(base + (k >> 2) * C::kChunkBytes + (k & 3) * 32, 16, 1024);
+        if (C::kTail16 && k == C::kN128 * 4)
+          return ptx::sdesc(base + C::kN128 * C::kAtom128, 16, 8 * 32, ptx::kLayoutSW32);
+        return ptx::sdesc_sw128(base + (k >> 2) * C::kAtom128 + (k & 3) * 32, 16, 1024);
       };
-      // MN-major V tile: 16-key step k starts at row 16k; 64-column atoms are kChunkBytes apart.
+      // MN-major V tile: 16-key step k starts at row 16k; 64-column atoms are kAtom128 apart.
       auto vdesc = [&](int stage, int k) -> uint64_t {
-        return ptx::sdesc_sw128(sKVa + stage * C::kTileBytes + k * 16 * 128, C::kChunkBytes, 1024);
+        return ptx::sdesc_sw128(sKVa + stage * C::kTileBytes + k * 16 * 128, C::kAtom128, 1024);
+      };
+      auto vdesc16 = [&](int stage, int k) -> uint64_t {  // D=72 tail: 16 columns, 32B swizzle
+        return ptx::sdesc(sKVa + stage * C::kTileBytes + C::kN128 * C::kAtom128 + k * 16 * 32, 16,
+                          8 * 32, ptx::kLayoutSW32);
       };
       auto kv_wait = [&](int idx) -> int {
         const int stage = idx % C::kStages;
@@ -293,14 +326,18 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto qk = [&](int t, int sK) {
         const uint32_t qa = sQa + t * C::kTileBytes, ka = sKVa + sK * C::kTileBytes;
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k)
+        for (int k = 0; k < C::kDp / 16; ++k)
           ptx::mma_ss(tmem + C::col_s(t), kmaj(qa, k), kmaj(ka, k), idesc_qk, k > 0 ? 1u : 0u);
       };
       auto pv = [&](int t, int sV, bool acc) {
 #pragma unroll
-        for (int k = 0; k < kBlockN / 16; ++k)
+        for (int k = 0; k < kBlockN / 16; ++k) {
           ptx::mma_ts(tmem + C::col_o(t), tmem + C::col_s(t) + k * 8, vdesc(sV, k), idesc_pv,
                       (acc || k > 0) ? 1u : 0u);
+          if (C::kTail16)
+            ptx::mma_ts(tmem + C::col_o(t) + 64, tmem + C::col_s(t) + k * 8, vdesc16(sV, k),
+                        idesc_pv16, (acc || k > 0) ? 1u : 0u);
+        }
       };
 
       ptx::mbar_wait(q_full, 0);
@@ -370,6 +407,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
             ptx::tmem_st32(tO + c * 32, o);
           }
+          if (D % 32) {  // D = 72: columns 64..71 (64..79 of the padded O hold zeros)
+            uint32_t o[8];
+            ptx::tmem_ld8(tO + (D / 32) * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+            ptx::tmem_st8(tO + (D / 32) * 32, o);
+          }
           m_used = m_new;
         }
       }
@@ -411,6 +456,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (D % 32) {  // D = 72 tail columns 64..71
+      uint32_t o[8];
+      ptx::tmem_ld8(tO + (D / 32) * 32, o);
+      ptx::tmem_ld_wait();
+      if (valid) {
+        if (p.out_f32) {
+          float4* dstp = reinterpret_cast<float4*>(static_cast<float*>(p.o) + dst.o_off + (D / 32) * 32);
+          dstp[0] = make_float4(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l, u2f(o[2]) * inv_l, u2f(o[3]) * inv_l);
+          dstp[1] = make_float4(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l, u2f(o[6]) * inv_l, u2f(o[7]) * inv_l);
+        } else {
+          uint4* dstp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.o) + dst.o_off + (D / 32) * 32);
+          dstp[0] = make_uint4(ptx::pack_bf16x2(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l),
+                               ptx::pack_bf16x2(u2f(o[2]) * inv_l, u2f(o[3]) * inv_l),
+                               ptx::pack_bf16x2(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l),
+                               ptx::pack_bf16x2(u2f(o[6]) * inv_l, u2f(o[7]) * inv_l));
+        }
+      }
+    }
     if (valid && p.lse) p.lse[dst.l_off] = (m_used + log2f(l)) * 0.69314718055994530942f;
   }
   __syncwarp();
@@ -434,24 +497,25 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
   return fn;
 }
 
-// [B][S][H][D] bf16 view with element strides (sb, ss, sh); box = 64 columns x 128 rows.
+// [B][S][H][D] bf16 view with element strides (sb, ss, sh); box = box_cols columns x 128 rows
+// (64 columns / 128B swizzle, or 16 columns / 32B swizzle for the D=72 tail atom).
 bool make_map(CUtensorMap* map, const void* base, int B, int S, int H, int D, int64_t sb, int64_t ss,
-              int64_t sh) {
+              int64_t sh, int box_cols = 64) {
   auto enc = get_encode_fn();
   if (!enc) return false;
   cuuint64_t dims[4] = {cuuint64_t(D), cuuint64_t(H), cuuint64_t(S), cuuint64_t(B)};
   cuuint64_t strides[3] = {cuuint64_t(sh * 2), cuuint64_t(ss * 2), cuuint64_t(sb * 2)};
-  cuuint32_t box[4] = {64, 1, 128, 1};
+  cuuint32_t box[4] = {cuuint32_t(box_cols), 1, 128, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
 
 template <int D, int EMU>
-cudaError_t launch_kernel(dim3 grid, const CUtensorMap& mq, const CUtensorMap& mk, const CUtensorMap& mv,
-                          const EpiParams& p, cudaStream_t st) {
+cudaError_t launch_kernel(dim3 grid, const CUtensorMap* m, const EpiParams& p, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_sm100_kernel<D, EMU>,
@@ -459,7 +523,8 @@ cudaError_t launch_kernel(dim3 grid, const CUtensorMap& mq, const CUtensorMap& m
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  attn_fwd_sm100_kernel<D, EMU><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(mq, mk, mv, p);
+  attn_fwd_sm100_kernel<D, EMU><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(m[0], m[1], m[2], m[3], m[4],
+                                                                           m[5], p);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -467,11 +532,21 @@ cudaError_t launch_kernel(dim3 grid, const CUtensorMap& mq, const CUtensorMap& m
 template <int D>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   using C = Cfg<D>;
-  CUtensorMap mq, mk, mv;
-  if (!make_map(&mq, a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h) ||
-      !make_map(&mk, a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h) ||
-      !make_map(&mv, a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h))
+  CUtensorMap m[6];
+  if (!make_map(&m[0], a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h) ||
+      !make_map(&m[1], a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h) ||
+      !make_map(&m[2], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h))
     return cudaErrorInvalidValue;
+  if (C::kTail16) {
+    if (!make_map(&m[3], a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h, 16) ||
+        !make_map(&m[4], a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 16) ||
+        !make_map(&m[5], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 16))
+      return cudaErrorInvalidValue;
+  } else {
+    m[3] = m[0];
+    m[4] = m[1];
+    m[5] = m[2];
+  }
   EpiParams p;
   p.o = a.o;
   p.lse = a.lse;
@@ -493,10 +568,10 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     return e ? std::atoi(e) : kDefaultEmu;
   }();
   switch (emu) {
-    case 0: return launch_kernel<D, 0>(grid, mq, mk, mv, p, st);
-    case 2: return launch_kernel<D, 2>(grid, mq, mk, mv, p, st);
-    case 4: return launch_kernel<D, 4>(grid, mq, mk, mv, p, st);
-    default: return launch_kernel<D, 3>(grid, mq, mk, mv, p, st);
+    case 0: return launch_kernel<D, 0>(grid, m, p, st);
+    case 2: return launch_kernel<D, 2>(grid, m, p, st);
+    case 4: return launch_kernel<D, 4>(grid, m, p, st);
+    default: return launch_kernel<D, 3>(grid, m, p, st);
   }
 }
 
@@ -506,6 +581,7 @@ cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st) {
   if (a.Sq == 0 || a.B == 0) return cudaSuccess;
   switch (a.D) {
     case 64: return launch_d<64>(a, st);
+    case 72: return launch_d<72>(a, st);
     case 128: return launch_d<128>(a, st);
     default: return cudaErrorInvalidValue;
   }

@@ -263,8 +263,8 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     return fail(XDIT_ERR_COMM_MISMATCH, "(ulysses=%d, ring=%d) does not match the handle (%d, %d, n=%d)",
                 u, r, c->u, c->r, c->nranks);
   const int dtype = eb == 2 ? 0 : 1;
-  if (dtype == 0 && D != 64 && D != 128)
-    return fail(XDIT_ERR_UNSUPPORTED, "bf16 path supports D in {64,128}, got %d", D);
+  if (dtype == 0 && D != 64 && D != 72 && D != 128)
+    return fail(XDIT_ERR_UNSUPPORTED, "bf16 path supports D in {64,72,128}, got %d", D);
   if (dtype == 1 && (D < 1 || D > 256))
     return fail(XDIT_ERR_UNSUPPORTED, "fp32 path supports D in [1,256], got %d", D);
   if (dtype == 1 && u * r > 1 && (D % 4) != 0)
@@ -610,7 +610,7 @@ int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* l
   if (dtype != 0 && dtype != 1) return fail(XDIT_ERR_UNSUPPORTED, "dtype must be 0 (bf16) or 1 (fp32)");
   XRET(check_map(omap, Sq));
   if (dtype == 0) {
-    if (D != 64 && D != 128) return fail(XDIT_ERR_UNSUPPORTED, "bf16 kernel supports D in {64,128}, got %d", D);
+    if (D != 64 && D != 72 && D != 128) return fail(XDIT_ERR_UNSUPPORTED, "bf16 kernel supports D in {64,72,128}, got %d", D);
     if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(o))
       return fail(XDIT_ERR_ALIGNMENT, "q/k/v/o must be 16-byte aligned");
     const int64_t st[6] = {q_b, q_s, q_h, kv_b, kv_s, kv_h};

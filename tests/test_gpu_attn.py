@@ -38,6 +38,8 @@ SHAPES = [  # B, H, Sq, Skv, D
     (1, 1, 1, 5, 64),
     (2, 2, 513, 127, 128),
     (1, 4, 1024, 1024, 64),
+    (2, 2, 300, 333, 72),
+    (1, 3, 256, 1000, 72),
 ]
 
 

@@ -29,7 +29,8 @@ def local_index(S_txt, S_img, N, g):
 
 
 # ------------------------------------------------------------------------------ N = 1 via the ABI
-@pytest.mark.parametrize("B,H,S_txt,S_img,D", [(1, 4, 0, 1024, 64), (2, 3, 33, 400, 64), (1, 2, 17, 300, 128)])
+@pytest.mark.parametrize("B,H,S_txt,S_img,D", [(1, 4, 0, 1024, 64), (2, 3, 33, 400, 64), (1, 2, 17, 300, 128),
+                                             (2, 4, 0, 520, 72)])
 @pytest.mark.parametrize("with_lse", [True, False])
 def test_usp_n1_full(B, H, S_txt, S_img, D, with_lse):
     S = S_txt + S_img
@@ -71,7 +72,7 @@ def test_usp_n1_errors():
         assert e.value.status == "DIVISIBILITY"
 
 
-@pytest.mark.parametrize("name", ["flux", "cogvideox", "sd3"])
+@pytest.mark.parametrize("name", ["flux", "cogvideox", "sd3", "pixart"])
 def test_usp_n1_full_size_sampled(name):
     """BASELINE.json full sizes, launch configuration of bench.py (N=1), sampled rows x 2 heads."""
     w = WORKLOADS[name]
@@ -214,7 +215,7 @@ SPLITS = [(2, 1), (1, 2), (4, 1), (2, 2), (1, 4), (8, 1), (4, 2), (2, 4), (1, 8)
 
 
 @pytest.mark.parametrize("u,r", SPLITS, ids=lambda x: str(x))
-@pytest.mark.parametrize("B,H,S_txt,S_img,D", [(2, 8, 33, 400, 64), (1, 8, 0, 1024, 128)])
+@pytest.mark.parametrize("B,H,S_txt,S_img,D", [(2, 8, 33, 400, 64), (1, 8, 0, 1024, 128), (2, 8, 0, 700, 72)])
 def test_virtual_usp_bf16(u, r, B, H, S_txt, S_img, D):
     S = S_txt + S_img
     q, k, v = qkv(B, S, H, D, seed=100 + u * 10 + r)
