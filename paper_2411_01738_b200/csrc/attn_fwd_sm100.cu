@@ -38,10 +38,12 @@ namespace {
 constexpr int kBlockM = 128;      // query rows per tile (= TMEM lanes)
 constexpr int kQTiles = 2;        // query tiles per CTA
 constexpr int kBlockN = 128;      // keys per KV tile
-constexpr int kThreads = 320;     // 8 softmax warps + TMA warp + MMA warp
+constexpr int kThreads = 384;     // 2 softmax warpgroups + 1 warpgroup {TMA, MMA, 2 spare warps}
+constexpr uint32_t kRegsSoftmax = 216, kRegsOther = 72;  // setmaxnreg split of 384 x 168 registers
 constexpr int kWarpTma = 8;
 constexpr int kWarpMma = 9;
 constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only if the max grows by > 2^8
+constexpr float kRedoThresh = 64.0f;    // log2 units: recompute a tile whose P would exceed 2^64
 constexpr uint32_t kTmemCols = 512;
 constexpr int kDefaultEmu = 3;  // exp2 pairs (of every 8) evaluated by polynomial on the FMA pipe
 
@@ -73,7 +75,15 @@ struct EpiParams {
   int H, Sq, Skv, out_f32;
   float scale_log2;
   int diag;  // profiling only (XDIT_DIAG): 1 = softmax does no math, 2 = also no MMA<-softmax wait
+  unsigned long long* trace;  // profiling only (XDIT_TRACE): per-iteration clock64 stamps of CTA 0
 };
+
+constexpr int kTraceIters = 64, kTraceEv = 10;
+__device__ __forceinline__ void stamp(const EpiParams& p, int j, int ev) {
+  if (p.trace && j < kTraceIters && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
+      (threadIdx.x & 31) == 0)
+    p.trace[j * kTraceEv + ev] = clock64();
+}
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
 __device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
@@ -205,6 +215,54 @@ __device__ __forceinline__ float exp_store_p(uint32_t tS, int valid, float sl2, 
   return (s0 + s1) + (s2 + s3);
 }
 
+// One pass over the tile: P = exp2(S * scale*log2e - m) for all 128 keys into 64 packed bf16x2
+// registers (nothing is written to TMEM yet, so S stays intact for a redo), the fp32 row sum of P
+// and the row max of the raw scores.  The two 64-column halves are read with two LDTM each.
+template <bool MASK, int EMU>
+__device__ __forceinline__ void exp_tile_regs(uint32_t tS, int valid, float sl2, float neg_m,
+                                              uint32_t (&pk)[64], float& rs, float& mx) {
+  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(neg_m, neg_m);
+  uint64_t acc0 = pk2(0.f, 0.f), acc1 = acc0;
+  float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+  for (int half = 0; half < 2; ++half) {
+    uint32_t a[32], bq[32];
+    ptx::tmem_ld32(tS + half * 64, a);
+    ptx::tmem_ld32(tS + half * 64 + 32, bq);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const uint32_t* src = (i < 16) ? a : bq;
+      const int e = (i & 15) * 2, col = half * 64 + (i < 16 ? 0 : 32) + e;
+      float s0 = u2f(src[e]), s1 = u2f(src[e + 1]);
+      if (MASK) {
+        if (col >= valid) s0 = -INFINITY;
+        if (col + 1 >= valid) s1 = -INFINITY;
+      }
+      if (i & 1) m1 = fmax3(m1, s0, s1);
+      else m0 = fmax3(m0, s0, s1);
+      const uint64_t x = fma2(pk2(s0, s1), sc2, nm2);
+      float p0, p1;
+      if (!MASK && (i & 7) < EMU) {
+        up2(exp2_poly2(x), p0, p1);
+      } else {
+        float x0, x1;
+        up2(x, x0, x1);
+        p0 = ptx::ex2(x0);
+        p1 = ptx::ex2(x1);
+      }
+      if (i & 1) acc1 = add2(acc1, pk2(p0, p1));
+      else acc0 = add2(acc0, pk2(p0, p1));
+      pk[half * 32 + i] = ptx::pack_bf16x2(p0, p1);
+    }
+  }
+  float s0, s1, s2, s3;
+  up2(acc0, s0, s1);
+  up2(acc1, s2, s3);
+  rs = (s0 + s1) + (s2 + s3);
+  mx = fmaxf(m0, m1);
+}
+
 template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -265,39 +323,48 @@ __global__ void __launch_bounds__(kThreads, 1)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == kWarpTma) {
+  if (warp >= 8) {
+   // warpgroup 2: TMA producer (warp 8), MMA issuer (warp 9), two spare warps -- few registers
+   ptx::setmaxnreg_dec<kRegsOther>();
+   if (warp == kWarpTma) {
     // ===================================================== TMA producer
-    if (lane == 0) {
+    {  // converged warp; one elected lane issues (operands stay in the uniform datapath)
       const uint64_t pol_q = ptx::policy_evict_first();
       const uint64_t pol_kv = ptx::policy_evict_last();
-      ptx::mbar_expect_tx(q_full, kQTiles * C::kTileBytes);
-      for (int t = 0; t < kQTiles; ++t) {
-        for (int c = 0; c < C::kN128; ++c)
-          ptx::tma_load_4d(sQ + t * C::kTileBytes + c * C::kAtom128, &tmQ, q_full, c * 64, h,
-                           m0 + t * kBlockM, b, pol_q);
-        if (C::kTail16)
-          ptx::tma_load_4d(sQ + t * C::kTileBytes + C::kN128 * C::kAtom128, &tmQ16, q_full,
-                           C::kN128 * 64, h, m0 + t * kBlockM, b, pol_q);
+      if (ptx::elect_one()) {
+        ptx::mbar_expect_tx(q_full, kQTiles * C::kTileBytes);
+        for (int t = 0; t < kQTiles; ++t) {
+          for (int c = 0; c < C::kN128; ++c)
+            ptx::tma_load_4d(sQ + t * C::kTileBytes + c * C::kAtom128, &tmQ, q_full, c * 64, h,
+                             m0 + t * kBlockM, b, pol_q);
+          if (C::kTail16)
+            ptx::tma_load_4d(sQ + t * C::kTileBytes + C::kN128 * C::kAtom128, &tmQ16, q_full,
+                             C::kN128 * 64, h, m0 + t * kBlockM, b, pol_q);
+        }
       }
+      __syncwarp();
       int it = 0;
       for (int j = 0; j < n_kv; ++j) {
         for (int kv = 0; kv < 2; ++kv, ++it) {
           const int stage = it % C::kStages, round = it / C::kStages;
           if (round > 0) ptx::mbar_wait(&kv_empty[stage], (round - 1) & 1);
-          ptx::mbar_expect_tx(&kv_full[stage], C::kTileBytes);
-          for (int c = 0; c < C::kN128; ++c)
-            ptx::tma_load_4d(sKV + stage * C::kTileBytes + c * C::kAtom128, kv ? &tmV : &tmK,
-                             &kv_full[stage], c * 64, h, j * kBlockN, b, pol_kv);
-          if (C::kTail16)
-            ptx::tma_load_4d(sKV + stage * C::kTileBytes + C::kN128 * C::kAtom128,
-                             kv ? &tmV16 : &tmK16, &kv_full[stage], C::kN128 * 64, h, j * kBlockN,
-                             b, pol_kv);
+          if (ptx::elect_one()) {
+            ptx::mbar_expect_tx(&kv_full[stage], C::kTileBytes);
+            for (int c = 0; c < C::kN128; ++c)
+              ptx::tma_load_4d(sKV + stage * C::kTileBytes + c * C::kAtom128, kv ? &tmV : &tmK,
+                               &kv_full[stage], c * 64, h, j * kBlockN, b, pol_kv);
+            if (C::kTail16)
+              ptx::tma_load_4d(sKV + stage * C::kTileBytes + C::kN128 * C::kAtom128,
+                               kv ? &tmV16 : &tmK16, &kv_full[stage], C::kN128 * 64, h, j * kBlockN,
+                               b, pol_kv);
+          }
+          __syncwarp();
         }
       }
     }
   } else if (warp == kWarpMma) {
     // ===================================================== MMA issuer (single thread)
-    if (lane == 0) {
+    {
       constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(kBlockM, kBlockN, 0, 0);
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(kBlockM, C::kTail16 ? 64 : D, 0, 1);
       constexpr uint32_t idesc_pv16 = ptx::idesc_bf16_f32(kBlockM, 16, 0, 1);
@@ -345,31 +412,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       int sVprev = 0;
       for (int j = 0; j < n_kv; ++j) {
         const int sK = kv_wait(2 * j);
-        qk(0, sK);  // S0 = Q0 K_j^T
-        ptx::tc_commit(&s_full[0]);
+        stamp(p, j, 0);
+        if (ptx::elect_one()) {
+          qk(0, sK);  // S0 = Q0 K_j^T
+          ptx::tc_commit(&s_full[0]);
+        }
+        __syncwarp();
+        stamp(p, j, 1);
         if (j > 0) {  // O1 += P1(j-1) V_{j-1}
           if (p.diag < 2) ptx::mbar_wait(&p_full[1], (j - 1) & 1);
+          stamp(p, j, 2);
           ptx::tc_fence_after();
-          pv(1, sVprev, j - 1 > 0);
-          ptx::tc_commit(&kv_empty[sVprev]);
+          if (ptx::elect_one()) {
+            pv(1, sVprev, j - 1 > 0);
+            ptx::tc_commit(&kv_empty[sVprev]);
+          }
+          __syncwarp();
         }
-        qk(1, sK);  // S1 = Q1 K_j^T
-        ptx::tc_commit(&s_full[1]);
-        ptx::tc_commit(&kv_empty[sK]);
+        if (ptx::elect_one()) {
+          qk(1, sK);  // S1 = Q1 K_j^T
+          ptx::tc_commit(&s_full[1]);
+          ptx::tc_commit(&kv_empty[sK]);
+        }
+        __syncwarp();
         const int sV = kv_wait(2 * j + 1);
+        stamp(p, j, 3);
         if (p.diag < 2) ptx::mbar_wait(&p_full[0], j & 1);  // O0 += P0(j) V_j
+        stamp(p, j, 4);
         ptx::tc_fence_after();
-        pv(0, sV, j > 0);
-        if (j == n_kv - 1) ptx::tc_commit(&o_full[0]);
+        if (ptx::elect_one()) {
+          pv(0, sV, j > 0);
+          if (j == n_kv - 1) ptx::tc_commit(&o_full[0]);
+        }
+        __syncwarp();
         sVprev = sV;
       }
       if (p.diag < 2) ptx::mbar_wait(&p_full[1], (n_kv - 1) & 1);
       ptx::tc_fence_after();
-      pv(1, sVprev, n_kv - 1 > 0);
-      ptx::tc_commit(&o_full[1]);
-      ptx::tc_commit(&kv_empty[sVprev]);
+      if (ptx::elect_one()) {
+        pv(1, sVprev, n_kv - 1 > 0);
+        ptx::tc_commit(&o_full[1]);
+        ptx::tc_commit(&kv_empty[sVprev]);
+      }
+      __syncwarp();
     }
+   }
   } else {
+    ptx::setmaxnreg_inc<kRegsSoftmax>();
     // ===================================================== softmax warpgroups (tile t = warp/4)
     const int t = warp >> 2, wq = warp & 3;
     const int row_in_tile = wq * 32 + lane;
@@ -377,9 +466,33 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tS = tmem + C::col_s(t) + lane_off;
     const uint32_t tO = tmem + C::col_o(t) + lane_off;
     const float sl2 = p.scale_log2;
-    float m_used = 0.f, l = 0.f;
+    float m_used = 0.f, m_next = 0.f, l = 0.f;
+    // O and l <- O, l * 2^(m_used - m_new); m_used <- m_new (warp-collective TMEM ld/st of O).
+    auto rescale_o = [&](float m_new) {
+      const float alpha = ptx::ex2(m_used - m_new);
+      l *= alpha;
+#pragma unroll
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t o[32];
+        ptx::tmem_ld32(tO + c * 32, o);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+        ptx::tmem_st32(tO + c * 32, o);
+      }
+      if (D % 32) {  // D = 72: columns 64..71 (64..79 of the padded O hold zeros)
+        uint32_t o[8];
+        ptx::tmem_ld8(tO + (D / 32) * 32, o);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+        ptx::tmem_st8(tO + (D / 32) * 32, o);
+      }
+      m_used = m_new;
+    };
     for (int j = 0; j < n_kv; ++j) {
       ptx::mbar_wait(&s_full[t], j & 1);
+      if ((warp & 3) == 0 && lane == 0) stamp(p, j, 5 + 2 * t);
       ptx::tc_fence_after();
       if (p.diag) {  // profiling: measure the MMA/TMA skeleton without the softmax
         __syncwarp();
@@ -388,43 +501,35 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const bool ragged = (j == n_kv - 1) && (p.Skv - j * kBlockN < kBlockN);
       const int valid = p.Skv - j * kBlockN;  // ragged KV tail (reading C16)
-      const float mx = ragged ? row_max<true>(tS, valid) : row_max<false>(tS, valid);
-      const float m_tile = mx * sl2;
+      // Reading R1 (lazy max): P of tile j is computed against the running reference m_used in ONE
+      // pass over S (no separate max pass on the critical path); the tile max found on the way only
+      // moves m_used -- and rescales O and l -- before the NEXT tile, when it grew by more than
+      // 2^kRescaleThresh.  A tile whose max exceeds m_used by more than kRedoThresh (P would exceed
+      // 2^kRedoThresh) is recomputed against its own max: S is still intact in TMEM at that point.
       if (j == 0) {
-        m_used = m_tile;
-      } else {
-        const bool need = m_tile > m_used + kRescaleThresh;
-        if (__any_sync(0xffffffffu, need)) {
-          const float m_new = fmaxf(m_used, m_tile);
-          const float alpha = ptx::ex2(m_used - m_new);
-          l *= alpha;
-#pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t o[32];
-            ptx::tmem_ld32(tO + c * 32, o);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
-            ptx::tmem_st32(tO + c * 32, o);
-          }
-          if (D % 32) {  // D = 72: columns 64..71 (64..79 of the padded O hold zeros)
-            uint32_t o[8];
-            ptx::tmem_ld8(tO + (D / 32) * 32, o);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
-            ptx::tmem_st8(tO + (D / 32) * 32, o);
-          }
-          m_used = m_new;
-        }
+        m_used = (ragged ? row_max<true>(tS, valid) : row_max<false>(tS, valid)) * sl2;
+      } else if (__any_sync(0xffffffffu, m_next > m_used)) {
+        rescale_o(m_next);  // PV(j-1) is complete: s_full(j) was committed after it
       }
-      const float rs = ragged ? exp_store_p<true, 0>(tS, valid, sl2, -m_used)
-                              : exp_store_p<false, EMU>(tS, valid, sl2, -m_used);
+      uint32_t pk[64];
+      float rs, mx;
+      if (ragged) exp_tile_regs<true, 0>(tS, valid, sl2, -m_used, pk, rs, mx);
+      else exp_tile_regs<false, EMU>(tS, valid, sl2, -m_used, pk, rs, mx);
+      const float m_tile = mx * sl2;
+      if (__any_sync(0xffffffffu, m_tile > m_used + kRedoThresh)) {  // rare: redo this tile
+        rescale_o(fmaxf(m_used, m_tile));
+        if (ragged) exp_tile_regs<true, 0>(tS, valid, sl2, -m_used, pk, rs, mx);
+        else exp_tile_regs<false, EMU>(tS, valid, sl2, -m_used, pk, rs, mx);
+      }
+      m_next = (m_tile > m_used + kRescaleThresh) ? m_tile : m_used;
       l += rs;
+      ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
+      ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
       ptx::tmem_st_wait();
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+      if ((warp & 3) == 0 && lane == 0) stamp(p, j, 6 + 2 * t);
     }
     // ------------------------------------------------- epilogue: O / l, LSE
     ptx::mbar_wait(&o_full[t], 0);
@@ -561,18 +666,40 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     return e ? std::atoi(e) : 0;
   }();
   p.diag = diag;
+  static unsigned long long* trace = [] {
+    unsigned long long* t = nullptr;
+    if (std::getenv("XDIT_TRACE")) cudaMalloc(&t, sizeof(unsigned long long) * kTraceIters * kTraceEv);
+    return t;
+  }();
+  p.trace = trace;
+  if (trace) cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * kTraceIters * kTraceEv, st);
   dim3 grid((a.Sq + kQTiles * kBlockM - 1) / (kQTiles * kBlockM), a.H, a.B);
   // fraction of exp2 moved to the FMA pipe: EMU of every 8 column pairs (XDIT_EXP_EMU overrides)
   static const int emu = [] {
     const char* e = std::getenv("XDIT_EXP_EMU");
     return e ? std::atoi(e) : kDefaultEmu;
   }();
+  cudaError_t err;
   switch (emu) {
-    case 0: return launch_kernel<D, 0>(grid, m, p, st);
-    case 2: return launch_kernel<D, 2>(grid, m, p, st);
-    case 4: return launch_kernel<D, 4>(grid, m, p, st);
-    default: return launch_kernel<D, 3>(grid, m, p, st);
+    case 0: err = launch_kernel<D, 0>(grid, m, p, st); break;
+    case 2: err = launch_kernel<D, 2>(grid, m, p, st); break;
+    case 4: err = launch_kernel<D, 4>(grid, m, p, st); break;
+    default: err = launch_kernel<D, 3>(grid, m, p, st); break;
   }
+  if (trace) {  // profiling only: print CTA 0's stamps relative to its first K arrival
+    unsigned long long h[kTraceIters * kTraceEv];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[0];
+    fprintf(stderr, "j kready qk0iss p1seen p0wait p0seen | s0seen p0arr s1seen p1arr\n");
+    for (int j = 0; j < kTraceIters; ++j) {
+      fprintf(stderr, "%d", j);
+      for (int e = 0; e < 9; ++e)
+        fprintf(stderr, " %lld", h[j * kTraceEv + e] ? (long long)(h[j * kTraceEv + e] - t0) : -1LL);
+      fprintf(stderr, "\n");
+    }
+  }
+  return err;
 }
 
 }  // namespace
