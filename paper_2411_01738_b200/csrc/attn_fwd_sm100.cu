@@ -45,7 +45,9 @@ constexpr int kWarpMma = 9;
 constexpr float kRescaleThresh = 8.0f;  // log2 units: rescale O only if the max grows by > 2^8
 constexpr float kRedoThresh = 64.0f;    // log2 units: recompute a tile whose P would exceed 2^64
 constexpr uint32_t kTmemCols = 512;
-constexpr int kDefaultEmu = 3;  // exp2 pairs (of every 8) evaluated by polynomial on the FMA pipe
+// exp2 pairs (of every 8) evaluated by polynomial on the FMA pipe: D=128 is tensor/MUFU balanced and
+// gains nothing (profiles/r01_ncu_attn_flux.md), D <= 80 is MUFU-bound and gains ~12%.
+constexpr int default_emu(int D) { return D >= 128 ? 0 : 2; }
 
 template <int D>
 struct Cfg {
@@ -677,14 +679,14 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   // fraction of exp2 moved to the FMA pipe: EMU of every 8 column pairs (XDIT_EXP_EMU overrides)
   static const int emu = [] {
     const char* e = std::getenv("XDIT_EXP_EMU");
-    return e ? std::atoi(e) : kDefaultEmu;
+    return e ? std::atoi(e) : -1;
   }();
   cudaError_t err;
-  switch (emu) {
+  switch (emu >= 0 ? emu : default_emu(D)) {
     case 0: err = launch_kernel<D, 0>(grid, m, p, st); break;
-    case 2: err = launch_kernel<D, 2>(grid, m, p, st); break;
+    case 3: err = launch_kernel<D, 3>(grid, m, p, st); break;
     case 4: err = launch_kernel<D, 4>(grid, m, p, st); break;
-    default: err = launch_kernel<D, 3>(grid, m, p, st); break;
+    default: err = launch_kernel<D, 2>(grid, m, p, st); break;
   }
   if (trace) {  // profiling only: print CTA 0's stamps relative to its first K arrival
     unsigned long long h[kTraceIters * kTraceEv];
