@@ -254,3 +254,22 @@ def test_virtual_usp_deterministic():
     b, _ = run_virtual_usp(q, k, v, 10, 290, 2, 2)
     for (o1, l1), (o2, l2) in zip(a, b):
         assert torch.equal(o1, o2) and torch.equal(l1, l2)
+
+
+@pytest.mark.parametrize("u,r", [(8, 1), (2, 4), (1, 8)], ids=lambda x: str(x))
+def test_virtual_usp_flux_full_size_sampled(u, r):
+    """Flux.1 4096px (BASELINE.json configs[3]) split over 8 virtual ranks at full size: the exact
+    per-rank kernel launches of an 8-GPU USP call (pack, unpack, ring of attention + merge, final
+    write into the reverse exchange buffer, unpack), checked on sampled rows of two heads per rank."""
+    w = WORKLOADS["flux"]
+    q, k, v = qkv(w.B, w.S, w.H, w.D, seed=seed_for(w))  # CPU, bit-reproducible
+    outs, loc = run_virtual_usp(q, k, v, w.S_txt, w.S_img, u, r)
+    heads = [1, w.H - 2]
+    qs, ks, vs = (f64(t[:, :, heads]) for t in (q, k, v))
+    for g in (0, 3, 7):
+        o, l = outs[g]
+        L = o.shape[1]
+        pick = sample_rows(L, 24, extra=[63, 64, L - 1])
+        rows = loc[g][pick].numpy()
+        ref_o, ref_l = oracle.attention_rows(qs, ks, vs, rows)
+        assert_bf16(errors(o[:, pick.cuda()][:, :, heads], l[:, heads][:, :, pick.cuda()], ref_o, ref_l))
