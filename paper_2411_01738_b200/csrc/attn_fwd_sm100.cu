@@ -265,6 +265,51 @@ __device__ __forceinline__ void exp_tile_regs(uint32_t tS, int valid, float sl2,
   mx = fmaxf(m0, m1);
 }
 
+// One 64-column half of a 128-key tile: P = exp2(S * scale*log2e - m) for S columns
+// [col0, col0 + 64) into 32 packed bf16x2 registers (nothing written to TMEM yet, so the half can be
+// recomputed), the fp32 row sum of those P and the row max of the raw scores.
+template <bool MASK, int EMU>
+__device__ __forceinline__ void exp_half64(uint32_t tS, int col0, int valid, float sl2, float neg_m,
+                                           uint32_t (&pk)[32], float& rs, float& mx) {
+  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(neg_m, neg_m);
+  uint64_t acc0 = pk2(0.f, 0.f), acc1 = acc0;
+  float m0 = -INFINITY, m1 = -INFINITY;
+  uint32_t a[32], bq[32];
+  ptx::tmem_ld32(tS + col0, a);
+  ptx::tmem_ld32(tS + col0 + 32, bq);
+  ptx::tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const uint32_t* src = (i < 16) ? a : bq;
+    const int e = (i & 15) * 2, col = col0 + (i < 16 ? 0 : 32) + e;
+    float s0 = u2f(src[e]), s1 = u2f(src[e + 1]);
+    if (MASK) {
+      if (col >= valid) s0 = -INFINITY;
+      if (col + 1 >= valid) s1 = -INFINITY;
+    }
+    if (i & 1) m1 = fmax3(m1, s0, s1);
+    else m0 = fmax3(m0, s0, s1);
+    const uint64_t x = fma2(pk2(s0, s1), sc2, nm2);
+    float p0, p1;
+    if (!MASK && (i & 7) < EMU) {
+      up2(exp2_poly2(x), p0, p1);
+    } else {
+      float x0, x1;
+      up2(x, x0, x1);
+      p0 = ptx::ex2(x0);
+      p1 = ptx::ex2(x1);
+    }
+    if (i & 1) acc1 = add2(acc1, pk2(p0, p1));
+    else acc0 = add2(acc0, pk2(p0, p1));
+    pk[i] = ptx::pack_bf16x2(p0, p1);
+  }
+  float s0, s1, s2, s3;
+  up2(acc0, s0, s1);
+  up2(acc1, s2, s3);
+  rs = (s0 + s1) + (s2 + s3);
+  mx = fmaxf(m0, m1);
+}
+
 template <int D, int EMU>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_sm100_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -284,8 +329,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* kv_full = bars + 1;
   uint64_t* kv_empty = kv_full + C::kStages;
   uint64_t* s_full = kv_empty + C::kStages;
-  uint64_t* p_full = s_full + 2;
-  uint64_t* o_full = p_full + 2;
+  uint64_t* p_full = s_full + 2;             // [t][half]: P of keys [64 half, 64 half + 64) stored
+  uint64_t* o_half = p_full + 4;             // [t]: PV of the first key half of tile t completed
+  uint64_t* o_full = o_half + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -301,7 +347,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int t = 0; t < 2; ++t) {
       ptx::mbar_init(&s_full[t], 1);
-      ptx::mbar_init(&p_full[t], 4);  // one arrive per softmax warp
+      ptx::mbar_init(&p_full[2 * t], 4);  // one arrive per softmax warp
+      ptx::mbar_init(&p_full[2 * t + 1], 4);
+      ptx::mbar_init(&o_half[t], 1);
       ptx::mbar_init(&o_full[t], 1);
     }
     ptx::fence_mbar_init();
@@ -398,15 +446,32 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int k = 0; k < C::kDp / 16; ++k)
           ptx::mma_ss(tmem + C::col_s(t), kmaj(qa, k), kmaj(ka, k), idesc_qk, k > 0 ? 1u : 0u);
       };
-      auto pv = [&](int t, int sV, bool acc) {
+      // O_t += P_t V for key half hf (16-key steps 4hf .. 4hf+3)
+      auto pv = [&](int t, int sV, bool acc, int hf) {
 #pragma unroll
-        for (int k = 0; k < kBlockN / 16; ++k) {
+        for (int k = 4 * hf; k < 4 * hf + 4; ++k) {
           ptx::mma_ts(tmem + C::col_o(t), tmem + C::col_s(t) + k * 8, vdesc(sV, k), idesc_pv,
                       (acc || k > 0) ? 1u : 0u);
           if (C::kTail16)
             ptx::mma_ts(tmem + C::col_o(t) + 64, tmem + C::col_s(t) + k * 8, vdesc16(sV, k),
                         idesc_pv16, (acc || k > 0) ? 1u : 0u);
         }
+      };
+
+      // PV of tile t, step jj: first key half as soon as the softmax released it (then commit
+      // o_half so a rare mid-tile O rescale can wait for it), second half when released.
+      auto pv_tile = [&](int t, int sV, int jj) {
+        if (p.diag < 2) ptx::mbar_wait(&p_full[2 * t], jj & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          pv(t, sV, jj > 0, 0);
+          ptx::tc_commit(&o_half[t]);
+        }
+        __syncwarp();
+        if (p.diag < 2) ptx::mbar_wait(&p_full[2 * t + 1], jj & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) pv(t, sV, true, 1);
+        __syncwarp();
       };
 
       ptx::mbar_wait(q_full, 0);
@@ -421,14 +486,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         stamp(p, j, 1);
-        if (j > 0) {  // O1 += P1(j-1) V_{j-1}
-          if (p.diag < 2) ptx::mbar_wait(&p_full[1], (j - 1) & 1);
+        if (j > 0) {  // O1 += P1(j-1) V_{j-1}, key half by key half as the softmax releases them
+          pv_tile(1, sVprev, j - 1);
           stamp(p, j, 2);
-          ptx::tc_fence_after();
-          if (ptx::elect_one()) {
-            pv(1, sVprev, j - 1 > 0);
-            ptx::tc_commit(&kv_empty[sVprev]);
-          }
+          if (ptx::elect_one()) ptx::tc_commit(&kv_empty[sVprev]);
           __syncwarp();
         }
         if (ptx::elect_one()) {
@@ -439,20 +500,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         __syncwarp();
         const int sV = kv_wait(2 * j + 1);
         stamp(p, j, 3);
-        if (p.diag < 2) ptx::mbar_wait(&p_full[0], j & 1);  // O0 += P0(j) V_j
+        pv_tile(0, sV, j);  // O0 += P0(j) V_j
         stamp(p, j, 4);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          pv(0, sV, j > 0);
-          if (j == n_kv - 1) ptx::tc_commit(&o_full[0]);
+        if (j == n_kv - 1) {
+          if (ptx::elect_one()) ptx::tc_commit(&o_full[0]);
+          __syncwarp();
         }
-        __syncwarp();
         sVprev = sV;
       }
-      if (p.diag < 2) ptx::mbar_wait(&p_full[1], (n_kv - 1) & 1);
-      ptx::tc_fence_after();
+      pv_tile(1, sVprev, n_kv - 1);
       if (ptx::elect_one()) {
-        pv(1, sVprev, n_kv - 1 > 0);
         ptx::tc_commit(&o_full[1]);
         ptx::tc_commit(&kv_empty[sVprev]);
       }
@@ -498,7 +555,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       if (p.diag) {  // profiling: measure the MMA/TMA skeleton without the softmax
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&p_full[t]);
+        if (lane == 0) {
+          ptx::mbar_arrive(&p_full[2 * t]);
+          ptx::mbar_arrive(&p_full[2 * t + 1]);
+        }
         continue;
       }
       const bool ragged = (j == n_kv - 1) && (p.Skv - j * kBlockN < kBlockN);
@@ -513,24 +573,52 @@ __global__ void __launch_bounds__(kThreads, 1)
       } else if (__any_sync(0xffffffffu, m_next > m_used)) {
         rescale_o(m_next);  // PV(j-1) is complete: s_full(j) was committed after it
       }
-      uint32_t pk[64];
-      float rs, mx;
-      if (ragged) exp_tile_regs<true, 0>(tS, valid, sl2, -m_used, pk, rs, mx);
-      else exp_tile_regs<false, EMU>(tS, valid, sl2, -m_used, pk, rs, mx);
-      const float m_tile = mx * sl2;
-      if (__any_sync(0xffffffffu, m_tile > m_used + kRedoThresh)) {  // rare: redo this tile
-        rescale_o(fmaxf(m_used, m_tile));
-        if (ragged) exp_tile_regs<true, 0>(tS, valid, sl2, -m_used, pk, rs, mx);
-        else exp_tile_regs<false, EMU>(tS, valid, sl2, -m_used, pk, rs, mx);
+      // The tile is processed in two 64-key halves; P of the first half is stored and released to
+      // the MMA warp (p_full[t][0]) before the second half is computed, so the tensor core runs
+      // PV over keys 0..63 while the exps of keys 64..127 are still in flight.
+      float m_tile;
+      {
+        uint32_t pk[32];
+        float rs, mx;
+        if (ragged) exp_half64<true, 0>(tS, 0, valid, sl2, -m_used, pk, rs, mx);
+        else exp_half64<false, EMU>(tS, 0, valid, sl2, -m_used, pk, rs, mx);
+        if (__any_sync(0xffffffffu, mx * sl2 > m_used + kRedoThresh)) {  // rare: recompute
+          rescale_o(fmaxf(m_used, mx * sl2));  // PV(j-1) complete; PV(j) not issued yet
+          if (ragged) exp_half64<true, 0>(tS, 0, valid, sl2, -m_used, pk, rs, mx);
+          else exp_half64<false, EMU>(tS, 0, valid, sl2, -m_used, pk, rs, mx);
+        }
+        l += rs;
+        m_tile = mx * sl2;
+        ptx::tmem_st32(tS, pk);  // P keys 0..63 -> packed columns 0..31 (their scores are consumed)
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[2 * t]);
+      }
+      {
+        uint32_t pk[32];
+        float rs, mx;
+        if (ragged) exp_half64<true, 0>(tS, 64, valid, sl2, -m_used, pk, rs, mx);
+        else exp_half64<false, EMU>(tS, 64, valid, sl2, -m_used, pk, rs, mx);
+        if (__any_sync(0xffffffffu, mx * sl2 > m_used + kRedoThresh)) {  // rare: recompute
+          // O already received PV over keys 0..63: wait for it (o_half completes once per step and
+          // PV(j+1) cannot start before this warp arrives, so the parity wait is exact), then
+          // rescale O and l together and recompute this half against the new reference.
+          ptx::mbar_wait(&o_half[t], j & 1);
+          ptx::tc_fence_after();
+          rescale_o(fmaxf(m_used, mx * sl2));
+          if (ragged) exp_half64<true, 0>(tS, 64, valid, sl2, -m_used, pk, rs, mx);
+          else exp_half64<false, EMU>(tS, 64, valid, sl2, -m_used, pk, rs, mx);
+        }
+        l += rs;
+        m_tile = fmaxf(m_tile, mx * sl2);
+        ptx::tmem_st32(tS + 32, pk);  // P keys 64..127 -> packed columns 32..63
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&p_full[2 * t + 1]);
       }
       m_next = (m_tile > m_used + kRescaleThresh) ? m_tile : m_used;
-      l += rs;
-      ptx::tmem_st32(tS, *reinterpret_cast<uint32_t(*)[32]>(&pk[0]));
-      ptx::tmem_st32(tS + 32, *reinterpret_cast<uint32_t(*)[32]>(&pk[32]));
-      ptx::tmem_st_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&p_full[t]);
       if ((warp & 3) == 0 && lane == 0) stamp(p, j, 6 + 2 * t);
     }
     // ------------------------------------------------- epilogue: O / l, LSE
