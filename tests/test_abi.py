@@ -82,3 +82,11 @@ def test_comm_init_mismatch_is_rejected_without_gpu():
 
 def test_launch_counter_exported():
     assert usp.launch_count() >= 0
+
+
+def test_missing_extension_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback: without the built library the binding raises instead of computing."""
+    monkeypatch.setattr(usp, "_lib", None)
+    monkeypatch.setattr(usp, "LIB_PATH", str(tmp_path / "libxdit_usp.so"))
+    with pytest.raises(ImportError):
+        usp.shard(0, 16, 2, 0)

@@ -273,3 +273,25 @@ def test_virtual_usp_flux_full_size_sampled(u, r):
         rows = loc[g][pick].numpy()
         ref_o, ref_l = oracle.attention_rows(qs, ks, vs, rows)
         assert_bf16(errors(o[:, pick.cuda()][:, :, heads], l[:, heads][:, :, pick.cuda()], ref_o, ref_l))
+
+
+def test_usp_call_is_cuda_graph_capturable():
+    """The call never allocates nor synchronises the host (workspace is reserved up front), so it
+    can be captured in a CUDA graph and replayed; replays give the same bits as eager calls."""
+    B, H, S_txt, S_img, D = 1, 4, 31, 480, 128
+    q, k, v = (t.cuda() for t in qkv(B, S_txt + S_img, H, D, seed=21))
+    with usp.Comm(1, 1) as comm:
+        out = torch.empty_like(q)
+        lse = torch.empty((B, H, S_txt + S_img), dtype=torch.float32, device="cuda")
+        usp.attention(q, k, v, S_txt=S_txt, S_img=S_img, comm=comm, out=out, lse=lse)  # reserve + warm up
+        torch.cuda.synchronize()
+        ref_o, ref_l = out.clone(), lse.clone()
+        out.zero_(); lse.zero_()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                usp.attention(q, k, v, S_txt=S_txt, S_img=S_img, comm=comm, out=out, lse=lse)
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_o) and torch.equal(lse, ref_l)
