@@ -295,3 +295,41 @@ def test_usp_call_is_cuda_graph_capturable():
         g.replay()
         torch.cuda.synchronize()
         assert torch.equal(out, ref_o) and torch.equal(lse, ref_l)
+
+
+@pytest.mark.parametrize("u,r,S_txt,S_img", [(2, 2, 3, 200), (1, 4, 2, 130), (4, 1, 0, 9), (2, 2, 5, 0)],
+                         ids=["txt<N", "txt<N-ring", "tiny", "text-only"])
+def test_virtual_usp_degenerate_shards(u, r, S_txt, S_img):
+    """Shards where some ranks hold no text tokens, a tiny sequence (ragged rows of 2-3 tokens per
+    rank) and a text-only sequence (reading C5: only an EMPTY shard is an error)."""
+    B, H, D = 2, 4, 64
+    q, k, v = qkv(B, S_txt + S_img, H, D, seed=77 + u + r)
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    outs, loc = run_virtual_usp(q, k, v, S_txt, S_img, u, r)
+    for g, (o, l) in enumerate(outs):
+        idx = loc[g].numpy()
+        assert_bf16(errors(o, l, ref_o[:, idx], ref_l[:, :, idx]))
+
+
+def test_virtual_usp_peaky_ring_merge():
+    """Large-magnitude scores (q, k x3, so logits x9): ring partials with very different LSEs must
+    merge exactly; V stays unit-normal so the north_star gates apply unchanged."""
+    B, H, D, S_txt, S_img = 1, 4, 128, 40, 600
+    q, k, _ = qkv(B, S_txt + S_img, H, D, seed=91, scale=3.0)
+    _, _, v = qkv(B, S_txt + S_img, H, D, seed=92)
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    outs, loc = run_virtual_usp(q, k, v, S_txt, S_img, 1, 4)
+    for g, (o, l) in enumerate(outs):
+        idx = loc[g].numpy()
+        e = errors(o, l, ref_o[:, idx], ref_l[:, :, idx])
+        assert e["o_maxabs"] <= 2e-2 and e["o_rell2"] <= 1e-2 and e["lse_maxabs"] <= 1e-3, e
+
+
+def test_usp_n1_single_token():
+    q, k, v = (t.cuda() for t in qkv(1, 1, 2, 64, seed=5))
+    with usp.Comm(1, 1) as comm:
+        out, lse = usp.attention(q, k, v, S_txt=0, S_img=1, comm=comm)
+        torch.cuda.synchronize()
+    assert torch.equal(out, v)  # one key: O = V exactly (SPEC S:72)
+    s = float((q.float() * k.float()).sum()) / 8.0
+    assert abs(float(lse[0, 0, 0]) - (float((q[0, 0, 0].float() * k[0, 0, 0].float()).sum()) / 8.0)) < 1e-5
