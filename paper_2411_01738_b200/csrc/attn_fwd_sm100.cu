@@ -269,15 +269,12 @@ __device__ __forceinline__ void exp_tile_regs(uint32_t tS, int valid, float sl2,
 // [col0, col0 + 64) into 32 packed bf16x2 registers (nothing written to TMEM yet, so the half can be
 // recomputed), the fp32 row sum of those P and the row max of the raw scores.
 template <bool MASK, int EMU>
-__device__ __forceinline__ void exp_half64(uint32_t tS, int col0, int valid, float sl2, float neg_m,
-                                           uint32_t (&pk)[32], float& rs, float& mx) {
+__device__ __forceinline__ void exp_regs64(const uint32_t (&a)[32], const uint32_t (&bq)[32], int col0,
+                                           int valid, float sl2, float neg_m, uint32_t (&pk)[32],
+                                           float& rs, float& mx) {
   const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(neg_m, neg_m);
   uint64_t acc0 = pk2(0.f, 0.f), acc1 = acc0;
   float m0 = -INFINITY, m1 = -INFINITY;
-  uint32_t a[32], bq[32];
-  ptx::tmem_ld32(tS + col0, a);
-  ptx::tmem_ld32(tS + col0 + 32, bq);
-  ptx::tmem_ld_wait();
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const uint32_t* src = (i < 16) ? a : bq;
@@ -308,6 +305,16 @@ __device__ __forceinline__ void exp_half64(uint32_t tS, int col0, int valid, flo
   up2(acc1, s2, s3);
   rs = (s0 + s1) + (s2 + s3);
   mx = fmaxf(m0, m1);
+}
+
+template <bool MASK, int EMU>
+__device__ __forceinline__ void exp_half64(uint32_t tS, int col0, int valid, float sl2, float neg_m,
+                                           uint32_t (&pk)[32], float& rs, float& mx) {
+  uint32_t a[32], bq[32];
+  ptx::tmem_ld32(tS + col0, a);
+  ptx::tmem_ld32(tS + col0 + 32, bq);
+  ptx::tmem_ld_wait();
+  exp_regs64<MASK, EMU>(a, bq, col0, valid, sl2, neg_m, pk, rs, mx);
 }
 
 template <int D, int EMU>
@@ -577,11 +584,17 @@ __global__ void __launch_bounds__(kThreads, 1)
       // the MMA warp (p_full[t][0]) before the second half is computed, so the tensor core runs
       // PV over keys 0..63 while the exps of keys 64..127 are still in flight.
       float m_tile;
+      uint32_t s0a[32], s0b[32], s1a[32], s1b[32];  // all 128 scores, one TMEM round trip
+      ptx::tmem_ld32(tS, s0a);
+      ptx::tmem_ld32(tS + 32, s0b);
+      ptx::tmem_ld32(tS + 64, s1a);
+      ptx::tmem_ld32(tS + 96, s1b);
+      ptx::tmem_ld_wait();
       {
         uint32_t pk[32];
         float rs, mx;
-        if (ragged) exp_half64<true, 0>(tS, 0, valid, sl2, -m_used, pk, rs, mx);
-        else exp_half64<false, EMU>(tS, 0, valid, sl2, -m_used, pk, rs, mx);
+        if (ragged) exp_regs64<true, 0>(s0a, s0b, 0, valid, sl2, -m_used, pk, rs, mx);
+        else exp_regs64<false, EMU>(s0a, s0b, 0, valid, sl2, -m_used, pk, rs, mx);
         if (__any_sync(0xffffffffu, mx * sl2 > m_used + kRedoThresh)) {  // rare: recompute
           rescale_o(fmaxf(m_used, mx * sl2));  // PV(j-1) complete; PV(j) not issued yet
           if (ragged) exp_half64<true, 0>(tS, 0, valid, sl2, -m_used, pk, rs, mx);
@@ -598,8 +611,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       {
         uint32_t pk[32];
         float rs, mx;
-        if (ragged) exp_half64<true, 0>(tS, 64, valid, sl2, -m_used, pk, rs, mx);
-        else exp_half64<false, EMU>(tS, 64, valid, sl2, -m_used, pk, rs, mx);
+        if (ragged) exp_regs64<true, 0>(s1a, s1b, 64, valid, sl2, -m_used, pk, rs, mx);
+        else exp_regs64<false, EMU>(s1a, s1b, 64, valid, sl2, -m_used, pk, rs, mx);
         if (__any_sync(0xffffffffu, mx * sl2 > m_used + kRedoThresh)) {  // rare: recompute
           // O already received PV over keys 0..63: wait for it (o_half completes once per step and
           // PV(j+1) cannot start before this warp arrives, so the parity wait is exact), then
