@@ -285,11 +285,12 @@ def main():
     ko = torch.empty_like(kq)
     kl = torch.empty((B, Hh, Sb), dtype=torch.float32, device=dev)
     kmap = usp.RowMap.plain(B, Sb, Hh, w.D)
+    kscr = torch.empty(usp.attn_scratch_bytes(w.D) // 4, dtype=torch.float32, device=dev)
 
-    def kern():
+    def kern():  # same launch configuration as inside the USP call (tail split enabled)
         usp.attn_fwd(kq, kk, kv_, ko, kl, B=B, H=Hh, Sq=Sb, Skv=Sb, D=w.D,
                      q_strides=(Sb * Hh * w.D, Hh * w.D, w.D), kv_strides=(Sb * Hh * w.D, Hh * w.D, w.D),
-                     omap=kmap)
+                     omap=kmap, scratch=kscr)
     for _ in range(2):
         kern()
     torch.cuda.synchronize()

@@ -198,11 +198,18 @@ typedef struct xdit_rowmap {
  * (D in {64,72,128}; q,k,v 16-byte aligned, strides multiples of 8 elements), 1 = fp32 inputs on the
  * SIMT kernel (D in [1,256]).  out_f32: 0 writes O as bf16 through `omap` (final output);
  * 1 writes O as fp32 through `omap` (ring partial).  lse may be NULL (skipped).
+ * scratch: optional 16-byte aligned DEVICE buffer of scratch_bytes (>= xdit_attn_scratch_bytes(D)
+ * to be used) that lets the bf16 kernel split the last, partial wave of its grid over key ranges
+ * (merged by an LSE-weighted tail kernel); NULL runs every work item over all keys.  Results are
+ * the same within rounding either way.
  * Errors: INVALID_ARG, UNSUPPORTED, ALIGNMENT, CUDA. */
 XDIT_API int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,
                   int Sq, int Skv, int D, int64_t q_b, int64_t q_s, int64_t q_h, int64_t kv_b,
                   int64_t kv_s, int64_t kv_h, const xdit_rowmap* omap, int dtype, int out_f32,
-                  xdit_stream_t stream);
+                  void* scratch, size_t scratch_bytes, xdit_stream_t stream);
+
+/* Scratch bytes xdit_attn_fwd can use for head dim D on the current device (0 for D <= 0). */
+XDIT_API size_t xdit_attn_scratch_bytes(int D);
 
 /* Ring partial-output merge ("parallel version of Flash Attention").
  * o_acc, o_s: fp32 [B][S][Hh][D] contiguous; lse_acc, lse_s: fp32 [B][Hh][S].

@@ -25,6 +25,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -76,6 +77,12 @@ struct EpiParams {
   xdit_rowmap map;
   int H, Sq, Skv, out_f32;
   float scale_log2;
+  // Work decomposition (1-D grid): items are (query-tile pair, head, batch), query tile fastest.
+  // Items [0, n_full) run over all keys; each of the remaining n_tail items is split into n_split
+  // key ranges of kv_chunk keys whose normalised fp32 partials (O, LSE) go to `part` and are merged
+  // by tail_merge_kernel -- this fills the last, partial wave of the grid.
+  int n_qt, n_full, n_split, kv_chunk;
+  float* part;  // [n_tail * n_split][256][D] fp32 O, then [n_tail * n_split][256] fp32 LSE
   int diag;  // profiling only (XDIT_DIAG): 1 = softmax does no math, 2 = also no MMA<-softmax wait
   unsigned long long* trace;  // profiling only (XDIT_TRACE): per-iteration clock64 stamps of CTA 0
 };
@@ -342,9 +349,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int h = blockIdx.y, b = blockIdx.z;
-  const int m0 = blockIdx.x * (kQTiles * kBlockM);
-  const int n_kv = (p.Skv + kBlockN - 1) / kBlockN;
+  int item = blockIdx.x, kv0 = 0, kv_len = p.Skv, piece = -1;
+  if (item >= p.n_full) {  // tail item: one key range of a split (query-tile pair, head, batch)
+    const int r = item - p.n_full;
+    piece = r;
+    item = p.n_full + r / p.n_split;
+    kv0 = (r % p.n_split) * p.kv_chunk;
+    kv_len = min(p.kv_chunk, p.Skv - kv0);
+  }
+  const int hb = item / p.n_qt, h = hb % p.H, b = hb / p.H;
+  const int m0 = (item % p.n_qt) * (kQTiles * kBlockM);
+  const int n_kv = (kv_len + kBlockN - 1) / kBlockN;
 
   if (threadIdx.x == 0) {
     ptx::mbar_init(q_full, 1);
@@ -409,10 +424,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_expect_tx(&kv_full[stage], C::kTileBytes);
             for (int c = 0; c < C::kN128; ++c)
               ptx::tma_load_4d(sKV + stage * C::kTileBytes + c * C::kAtom128, kv ? &tmV : &tmK,
-                               &kv_full[stage], c * 64, h, j * kBlockN, b, pol_kv);
+                               &kv_full[stage], c * 64, h, kv0 + j * kBlockN, b, pol_kv);
             if (C::kTail16)
               ptx::tma_load_4d(sKV + stage * C::kTileBytes + C::kN128 * C::kAtom128,
-                               kv ? &tmV16 : &tmK16, &kv_full[stage], C::kN128 * 64, h, j * kBlockN,
+                               kv ? &tmV16 : &tmK16, &kv_full[stage], C::kN128 * 64, h, kv0 + j * kBlockN,
                                b, pol_kv);
           }
           __syncwarp();
@@ -568,8 +583,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         continue;
       }
-      const bool ragged = (j == n_kv - 1) && (p.Skv - j * kBlockN < kBlockN);
-      const int valid = p.Skv - j * kBlockN;  // ragged KV tail (reading C16)
+      const bool ragged = (j == n_kv - 1) && (kv_len - j * kBlockN < kBlockN);
+      const int valid = kv_len - j * kBlockN;  // ragged KV tail of this key range (reading C16)
       // Reading R1 (lazy max): P of tile j is computed against the running reference m_used in ONE
       // pass over S (no separate max pass on the critical path); the tile max found on the way only
       // moves m_used -- and rescales O and l -- before the NEXT tile, when it grew by more than
@@ -639,7 +654,19 @@ __global__ void __launch_bounds__(kThreads, 1)
     ptx::tc_fence_after();
     const int row = m0 + t * kBlockM + row_in_tile;
     const float inv_l = 1.f / l;
-    const RowDst dst = rowmap_dst(p.map, b, row, h);
+    RowDst dst = rowmap_dst(p.map, b, row, h);
+    void* obase = p.o;
+    float* lbase = p.lse;
+    int of32 = p.out_f32;
+    if (piece >= 0) {  // split tail item: normalised fp32 partial for tail_merge_kernel
+      const int64_t prow = int64_t(piece) * (kQTiles * kBlockM) + t * kBlockM + row_in_tile;
+      const int64_t n_pieces = int64_t(gridDim.x) - p.n_full;
+      obase = p.part;
+      lbase = p.part + n_pieces * (kQTiles * kBlockM) * D;
+      of32 = 1;
+      dst.o_off = prow * D;
+      dst.l_off = prow;
+    }
     const bool valid = row < p.Sq;
 #pragma unroll
     for (int c = 0; c < D / 32; ++c) {
@@ -647,14 +674,14 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_ld32(tO + c * 32, o);
       ptx::tmem_ld_wait();
       if (valid) {
-        if (p.out_f32) {
-          float4* dstp = reinterpret_cast<float4*>(static_cast<float*>(p.o) + dst.o_off + c * 32);
+        if (of32) {
+          float4* dstp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + c * 32);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
             dstp[i] = make_float4(u2f(o[4 * i]) * inv_l, u2f(o[4 * i + 1]) * inv_l,
                                   u2f(o[4 * i + 2]) * inv_l, u2f(o[4 * i + 3]) * inv_l);
         } else {
-          uint4* dstp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.o) + dst.o_off + c * 32);
+          uint4* dstp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + c * 32);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             dstp[i] = make_uint4(ptx::pack_bf16x2(u2f(o[8 * i]) * inv_l, u2f(o[8 * i + 1]) * inv_l),
@@ -669,12 +696,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_ld8(tO + (D / 32) * 32, o);
       ptx::tmem_ld_wait();
       if (valid) {
-        if (p.out_f32) {
-          float4* dstp = reinterpret_cast<float4*>(static_cast<float*>(p.o) + dst.o_off + (D / 32) * 32);
+        if (of32) {
+          float4* dstp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + (D / 32) * 32);
           dstp[0] = make_float4(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l, u2f(o[2]) * inv_l, u2f(o[3]) * inv_l);
           dstp[1] = make_float4(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l, u2f(o[6]) * inv_l, u2f(o[7]) * inv_l);
         } else {
-          uint4* dstp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(p.o) + dst.o_off + (D / 32) * 32);
+          uint4* dstp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + (D / 32) * 32);
           dstp[0] = make_uint4(ptx::pack_bf16x2(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l),
                                ptx::pack_bf16x2(u2f(o[2]) * inv_l, u2f(o[3]) * inv_l),
                                ptx::pack_bf16x2(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l),
@@ -682,13 +709,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-    if (valid && p.lse) p.lse[dst.l_off] = (m_used + log2f(l)) * 0.69314718055994530942f;
+    if (valid && lbase) lbase[dst.l_off] = (m_used + log2f(l)) * 0.69314718055994530942f;
   }
   __syncwarp();
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   if (warp == kWarpMma) ptx::tmem_dealloc(tmem, kTmemCols);
+}
+
+// Merge of the split tail items (LSE-weighted, as the ring merge a7): one warp per (tail item, row).
+template <int D>
+__global__ void __launch_bounds__(256)
+    tail_merge_kernel(const float* __restrict__ part, int n_tail, int n_split, int n_full, int n_qt,
+                      int H, int Sq, EpiParams p) {
+  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (w >= n_tail * (kQTiles * kBlockM)) return;
+  const int ti = w / (kQTiles * kBlockM), rr = w % (kQTiles * kBlockM);
+  const int item = n_full + ti, hb = item / n_qt, h = hb % H, b = hb / H;
+  const int row = (item % n_qt) * (kQTiles * kBlockM) + rr;
+  if (row >= Sq) return;
+  const int64_t n_pieces = int64_t(n_tail) * n_split;
+  const float* plse = part + n_pieces * (kQTiles * kBlockM) * D;
+  float M = -INFINITY;
+  for (int s = 0; s < n_split; ++s) M = fmaxf(M, plse[(int64_t(ti) * n_split + s) * (kQTiles * kBlockM) + rr]);
+  float sum = 0.f;
+  for (int s = 0; s < n_split; ++s) sum += expf(plse[(int64_t(ti) * n_split + s) * (kQTiles * kBlockM) + rr] - M);
+  const float L = M + logf(sum);
+  const RowDst dst = rowmap_dst(p.map, b, row, h);
+  for (int d = lane * 4; d < D; d += 128) {
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < n_split; ++s) {
+      const int64_t pr = (int64_t(ti) * n_split + s) * (kQTiles * kBlockM) + rr;
+      const float wgt = expf(plse[pr] - L);
+      const float4 x = *reinterpret_cast<const float4*>(part + pr * D + d);
+      acc.x += wgt * x.x; acc.y += wgt * x.y; acc.z += wgt * x.z; acc.w += wgt * x.w;
+    }
+    if (p.out_f32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(p.o) + dst.o_off + d) = acc;
+    } else {
+      uint2 v;
+      v.x = ptx::pack_bf16x2(acc.x, acc.y);
+      v.y = ptx::pack_bf16x2(acc.z, acc.w);
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.o) + dst.o_off + d) = v;
+    }
+  }
+  if (lane == 0 && p.lse) p.lse[dst.l_off] = L;
 }
 
 // ------------------------------------------------------------------ host side
@@ -776,7 +842,39 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   }();
   p.trace = trace;
   if (trace) cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * kTraceIters * kTraceEv, st);
-  dim3 grid((a.Sq + kQTiles * kBlockM - 1) / (kQTiles * kBlockM), a.H, a.B);
+  // 1-D grid over (query-tile pair, head, batch) items; split the last partial wave over key
+  // ranges when a scratch buffer is available (DESIGN.md §7.1 "tail split").
+  p.n_qt = (a.Sq + kQTiles * kBlockM - 1) / (kQTiles * kBlockM);
+  const int items = p.n_qt * a.H * a.B;
+  p.n_full = items;
+  p.n_split = 1;
+  p.kv_chunk = a.Skv;
+  p.part = nullptr;
+  int n_tail = 0;
+  static const int nsm = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n;
+  }();
+  static const bool no_split = std::getenv("XDIT_NO_TAIL_SPLIT") != nullptr;
+  if (a.scratch && !no_split && items > nsm && items % nsm) {
+    const int rem = items % nsm, n_kv_tiles = (a.Skv + kBlockN - 1) / kBlockN;
+    int ns = std::min(std::min(nsm / rem, 8), n_kv_tiles / 2);
+    if (ns >= 2) {
+      const int chunk = ((n_kv_tiles + ns - 1) / ns) * kBlockN;
+      ns = (a.Skv + chunk - 1) / chunk;
+      const size_t need = size_t(rem) * ns * (kQTiles * kBlockM) * (D + 1);
+      if (ns >= 2 && need <= a.scratch_floats) {
+        n_tail = rem;
+        p.n_full = items - rem;
+        p.n_split = ns;
+        p.kv_chunk = chunk;
+        p.part = a.scratch;
+      }
+    }
+  }
+  dim3 grid(p.n_full + n_tail * p.n_split);
   // fraction of exp2 moved to the FMA pipe: EMU of every 8 column pairs (XDIT_EXP_EMU overrides)
   static const int emu = [] {
     const char* e = std::getenv("XDIT_EXP_EMU");
@@ -788,6 +886,13 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     case 3: err = launch_kernel<D, 3>(grid, m, p, st); break;
     case 4: err = launch_kernel<D, 4>(grid, m, p, st); break;
     default: err = launch_kernel<D, 2>(grid, m, p, st); break;
+  }
+  if (err == cudaSuccess && n_tail) {
+    const int rows = n_tail * kQTiles * kBlockM;
+    tail_merge_kernel<D><<<(rows + 7) / 8, 256, 0, st>>>(p.part, n_tail, p.n_split, p.n_full, p.n_qt,
+                                                          a.H, a.Sq, p);
+    note_launches(1);
+    err = cudaGetLastError();
   }
   if (trace) {  // profiling only: print CTA 0's stamps relative to its first K arrival
     unsigned long long h[kTraceIters * kTraceEv];
@@ -806,6 +911,13 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+size_t attn_scratch_floats(int D) {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  return size_t(nsm) * (kQTiles * kBlockM) * size_t(D + 1);
+}
 
 cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st) {
   if (a.Sq == 0 || a.B == 0) return cudaSuccess;

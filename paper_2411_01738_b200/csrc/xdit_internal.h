@@ -24,7 +24,13 @@ struct AttnArgs {
   int64_t kv_b, kv_s, kv_h;
   xdit_rowmap omap;
   int out_f32;
+  float* scratch = nullptr;    // optional fp32 scratch for the tail split (bf16 kernel), may be null
+  size_t scratch_floats = 0;
 };
+
+// fp32 scratch the bf16 attention kernel can use to split the last partial wave of its grid:
+// (#SMs) x 256 rows x (D + 1) floats.
+size_t attn_scratch_floats(int D);
 
 // Launchers return cudaError_t (cudaSuccess on success); argument checks happen in xdit_usp.cpp.
 cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st);  // bf16, D in {64,128}

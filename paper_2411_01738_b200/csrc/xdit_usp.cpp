@@ -196,7 +196,7 @@ struct xdit_comm_s {
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_a2a = nullptr, ev_o = nullptr, ev_o_a2a = nullptr;
   cudaEvent_t ev_kdone[2] = {nullptr, nullptr}, ev_recv[2] = {nullptr, nullptr};
-  Buf uly_send, uly_recv, qblk, kv[2][2], oacc, lacc, otmp, ltmp, osend, orecv;
+  Buf uly_send, uly_recv, qblk, kv[2][2], oacc, lacc, otmp, ltmp, osend, orecv, tail;
 };
 
 namespace {
@@ -241,7 +241,12 @@ int a2a(ncclComm_t comm, int n, const void* send, void* recv, size_t chunk, cuda
   return XDIT_OK;
 }
 
-int attn_launch(const AttnArgs& a, int dtype, cudaStream_t st) {
+int attn_launch(const AttnArgs& a_in, int dtype, cudaStream_t st, const Buf* scratch = nullptr) {
+  AttnArgs a = a_in;
+  if (scratch && scratch->p) {
+    a.scratch = static_cast<float*>(scratch->p);
+    a.scratch_floats = scratch->bytes / sizeof(float);
+  }
   cudaError_t e = dtype == 0 ? xdit::launch_attn_fwd_sm100(a, st) : xdit::launch_attn_fwd_f32(a, st);
   if (e != cudaSuccess)
     return fail(XDIT_ERR_CUDA, "attention launch failed: %s", cudaGetErrorString(e));
@@ -292,7 +297,7 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     a.q_b = a.kv_b = int64_t(L) * H * D; a.q_s = a.kv_s = int64_t(H) * D; a.q_h = a.kv_h = D;
     a.omap = plain_map(B, L, H, D);
     a.out_f32 = dtype;
-    return attn_launch(a, dtype, st);
+    return attn_launch(a, dtype, st, &c->tail);
   }
 
   XCUDA(cudaEventRecord(c->ev_start, st));
@@ -351,7 +356,7 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     a.k = Kc; a.v = Vc; a.Skv = Sb;
     a.kv_b = q_b; a.kv_s = q_s; a.kv_h = D;
     a.o = dst; a.lse = dst_lse; a.omap = fmap; a.out_f32 = dtype;
-    XRET(attn_launch(a, dtype, st));
+    XRET(attn_launch(a, dtype, st, &c->tail));
   } else {
     // ---- a5-a7: ring loop; step s attends to the KV block of ring index (i - s) mod r (C9)
     const int nxt_peer = (i + 1) % P.r, prv_peer = (i - 1 + P.r) % P.r;
@@ -384,7 +389,7 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
       } else {
         a.o = c->otmp.p; a.lse = static_cast<float*>(c->ltmp.p);
       }
-      XRET(attn_launch(a, dtype, st));
+      XRET(attn_launch(a, dtype, st, &c->tail));
       if (s > 0) {
         const bool last = s == P.r - 1;
         XCUDA(xdit::launch_lse_merge(static_cast<float*>(c->oacc.p), static_cast<float*>(c->lacc.p),
@@ -556,6 +561,7 @@ int xdit_comm_reserve(xdit_comm_t c, int B, int H, int S_txt, int S_img, int D, 
   XRET(ensure(&c->ltmp, s.lacc));
   XRET(ensure(&c->osend, s.ochunk * P.u * (P.u > 1)));
   XRET(ensure(&c->orecv, s.ochunk * P.u * (P.u > 1)));
+  if (elem_bytes == 2) XRET(ensure(&c->tail, xdit::attn_scratch_floats(D) * sizeof(float)));
   return XDIT_OK;
 }
 
@@ -572,7 +578,7 @@ int xdit_comm_destroy(xdit_comm_t c) {
   if (!c) return XDIT_OK;
   if (c->side) cudaStreamSynchronize(c->side);
   Buf* bufs[] = {&c->uly_send, &c->uly_recv, &c->qblk, &c->kv[0][0], &c->kv[0][1], &c->kv[1][0],
-                 &c->kv[1][1], &c->oacc, &c->lacc, &c->otmp, &c->ltmp, &c->osend, &c->orecv};
+                 &c->kv[1][1], &c->oacc, &c->lacc, &c->otmp, &c->ltmp, &c->osend, &c->orecv, &c->tail};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->uly) ncclCommDestroy(c->uly);
@@ -604,7 +610,7 @@ int xdit_usp_attention_f32(const float* q, const float* k, const float* v, float
 int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,
                   int Sq, int Skv, int D, int64_t q_b, int64_t q_s, int64_t q_h, int64_t kv_b,
                   int64_t kv_s, int64_t kv_h, const xdit_rowmap* omap, int dtype, int out_f32,
-                  xdit_stream_t stream) {
+                  void* scratch, size_t scratch_bytes, xdit_stream_t stream) {
   if (!q || !k || !v || !o) return fail(XDIT_ERR_INVALID_ARG, "q/k/v/o must not be NULL");
   if (B < 0 || H <= 0 || Sq < 0 || Skv <= 0) return fail(XDIT_ERR_INVALID_ARG, "bad sizes");
   if (dtype != 0 && dtype != 1) return fail(XDIT_ERR_UNSUPPORTED, "dtype must be 0 (bf16) or 1 (fp32)");
@@ -626,7 +632,17 @@ int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* l
   a.q_b = q_b; a.q_s = q_s; a.q_h = q_h; a.kv_b = kv_b; a.kv_s = kv_s; a.kv_h = kv_h;
   a.omap = *omap;
   a.out_f32 = dtype == 1 ? 1 : out_f32;
+  if (scratch) {
+    if (!aligned16(scratch)) return fail(XDIT_ERR_ALIGNMENT, "scratch must be 16-byte aligned");
+    a.scratch = static_cast<float*>(scratch);
+    a.scratch_floats = scratch_bytes / sizeof(float);
+  }
   return attn_launch(a, dtype, reinterpret_cast<cudaStream_t>(stream));
+}
+
+size_t xdit_attn_scratch_bytes(int D) {
+  if (D <= 0) return 0;
+  return xdit::attn_scratch_floats(D) * sizeof(float);
 }
 
 int xdit_lse_merge(float* o_acc, float* lse_acc, const float* o_s, const float* lse_s, int B, int S,

@@ -71,7 +71,9 @@ _SIGS = {
     "xdit_comm_destroy": ([_vp], _i),
     "xdit_usp_attention": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
     "xdit_usp_attention_f32": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
-    "xdit_attn_fwd": ([_vp] * 5 + [_i] * 5 + [_i64] * 6 + [ctypes.POINTER(RowMap), _i, _i, _vp], _i),
+    "xdit_attn_fwd": ([_vp] * 5 + [_i] * 5 + [_i64] * 6 + [ctypes.POINTER(RowMap), _i, _i, _vp, ctypes.c_size_t,
+                                                            _vp], _i),
+    "xdit_attn_scratch_bytes": ([_i], ctypes.c_size_t),
     "xdit_lse_merge": ([_vp] * 4 + [_i] * 4 + [_vp, _vp, ctypes.POINTER(RowMap), _i, _vp], _i),
     "xdit_uly_pack": ([_vp, _vp] + [_i] * 9 + [_vp], _i),
     "xdit_uly_unpack": ([_vp, _vp] + [_i] * 5 + [ctypes.POINTER(_i), _i, _i, _i, _vp], _i),
@@ -227,12 +229,18 @@ def attention(q, k, v, *, S_txt: int, S_img: int, comm: Comm, ulysses: int = 1, 
 
 
 # ------------------------------------------------------------------------------------ stage kernels
+def attn_scratch_bytes(D: int) -> int:
+    return int(lib().xdit_attn_scratch_bytes(D))
+
+
 def attn_fwd(q, k, v, o, lse, *, B: int, H: int, Sq: int, Skv: int, D: int, q_strides, kv_strides,
-             omap: RowMap, dtype: int = 0, out_f32: int = 0, stream=None):
-    """One attention launch (see xdit_attn_fwd).  Strides are (b, s, h) in elements."""
+             omap: RowMap, dtype: int = 0, out_f32: int = 0, scratch=None, stream=None):
+    """One attention launch (see xdit_attn_fwd).  Strides are (b, s, h) in elements.  `scratch`
+    (a CUDA tensor of >= attn_scratch_bytes(D) bytes, or None) enables the tail split."""
+    nbytes = 0 if scratch is None else scratch.numel() * scratch.element_size()
     rc = lib().xdit_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), B, H, Sq, Skv, D,
                              *[int(x) for x in q_strides], *[int(x) for x in kv_strides],
-                             ctypes.byref(omap), dtype, out_f32, _stream(stream))
+                             ctypes.byref(omap), dtype, out_f32, _ptr(scratch), nbytes, _stream(stream))
     _check(rc, "xdit_attn_fwd")
 
 

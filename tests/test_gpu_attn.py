@@ -12,7 +12,7 @@ import torch
 
 import oracle
 from paper_2411_01738_b200 import usp
-from paper_2411_01738_b200.inputs import qkv
+from paper_2411_01738_b200.inputs import qkv, sample_rows
 from tests._util import assert_bf16, assert_f32, errors, f64
 
 pytestmark = pytest.mark.gpu
@@ -125,3 +125,30 @@ def test_unsupported_head_dim_is_rejected():
     with pytest.raises(usp.XditError) as ei:
         run_attn(q, q, q)
     assert ei.value.status == "UNSUPPORTED"
+
+
+@pytest.mark.parametrize("D", [64, 72, 128])
+@pytest.mark.parametrize("Skv", [4096, 1000])
+def test_attn_tail_split_vs_oracle(D, Skv):
+    """160 work items on 148 SMs: the last 12 (query-tile pair, head) items are split over key
+    ranges and merged by the tail kernel.  Rows of the split items and of full items both match."""
+    B, H, Sq = 1, 10, 4096
+    q, _, _ = qkv(B, Sq, H, D, seed=500 + D)
+    _, k, v = qkv(B, Skv, H, D, seed=600 + D)
+    qc, kc, vc = q.cuda(), k.cuda(), v.cuda()
+    o = torch.empty(q.shape, dtype=torch.bfloat16, device="cuda")
+    l = torch.empty((B, H, Sq), dtype=torch.float32, device="cuda")
+    scratch = torch.empty(usp.attn_scratch_bytes(D) // 4, dtype=torch.float32, device="cuda")
+    n0 = usp.launch_count()
+    usp.attn_fwd(qc, kc, vc, o, l, B=B, H=H, Sq=Sq, Skv=Skv, D=D, q_strides=(Sq * H * D, H * D, D),
+                 kv_strides=(Skv * H * D, H * D, D), omap=usp.RowMap.plain(B, Sq, H, D), scratch=scratch)
+    torch.cuda.synchronize()
+    launches = usp.launch_count() - n0
+    if torch.cuda.get_device_properties(0).multi_processor_count == 148:
+        assert launches == 2  # attention + tail merge
+    heads = [0, 8, 9]
+    rows = sample_rows(Sq, 64, extra=[1024, 1279, 1280, 4095, 3839, 3840])
+    ref_o, ref_l = oracle.attention_rows(f64(q[:, :, heads]), f64(k[:, :, heads]), f64(v[:, :, heads]), rows.numpy())
+    got_o = o[:, rows.cuda()][:, :, heads]
+    got_l = l[:, heads][:, :, rows.cuda()]
+    assert_bf16(errors(got_o, got_l, ref_o, ref_l))
