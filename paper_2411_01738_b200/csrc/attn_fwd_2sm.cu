@@ -1,0 +1,567 @@
+// attn_fwd_2sm.cu -- flash-attention forward on a CTA PAIR (cta_group::2) for B200 (sm_100a).
+//
+// Same operation as attn_fwd_sm100.cu (§4.1.1 / P:257 §4.1.2;
+// readings C1-C3, C10, R1): O = softmax(Q K^T / sqrt(D)) V and LSE for one (Q block, KV block).
+//
+// Why a second kernel (DESIGN.md §7 "CTA-pair kernel"): in the one-CTA kernel the S_t / P_t TMEM
+// columns alias, so QK^T of the next key tile of a query tile cannot start before the P.V of the
+// current one -- every step of a tile is a serial chain softmax -> PV -> QK^T, and the tensor core
+// idles ~40 % (profiles/r01_ncu_attn_flux.md).  Here the two SMs of a TPC run one 256-row work item
+// together with M = 256 MMAs, which frees TMEM for DOUBLE-BUFFERED S and P per SM:
+//   * CTA rank r owns query rows [128 r, 128 r + 128) of the item: its Q tile, its S/P/O in TMEM;
+//   * each CTA loads HALF of every K tile (keys [64 r, 64 r + 64)) and HALF of every V tile
+//     (head-dim columns [64 r, 64 r + 64)): the pair's MMAs read the other half from the peer SM,
+//     so L2->SM traffic per SM equals the one-CTA kernel's (two query tiles per K/V load) and the
+//     smem operand traffic per SM drops to 3/4 (QK^T) and 1/2 (PV);
+//   * the leader's MMA warp issues QK^T(j+1) into S[(j+1)%2] as soon as the softmax has loaded
+//     S(j-1) into registers -- before PV(j) -- so the tensor core always has the next QK^T queued
+//     while the softmax of step j runs; P(j) goes to P[j%2], free once PV(j-2) has completed;
+//   * 8 softmax warps per CTA, two per TMEM lane quarter: warp w handles rows 32 (w%4) .. +31 and
+//     key columns [64 (w/4), 64 (w/4) + 64).  The two halves of a row exchange their tile max
+//     through smem (named barrier per row quarter) and apply the same running max m: it moves --
+//     rescaling O and l -- only when the tile max exceeds it by more than 2^8 (so P <= 2^8 and no
+//     recomputation is ever needed); each half keeps a partial row sum, added in the epilogue.
+// TMEM per SM (512 columns): S[0] [0,128) S[1] [128,256) P[0] [256,320) P[1] [320,384) O [384,512).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+
+#include "attn_common.cuh"
+
+namespace xdit {
+namespace {
+
+namespace pair2 {
+
+constexpr int kThreads = 384;      // 8 softmax warps, TMA warp, MMA warp, 2 idle warps
+constexpr int kWarpTma = 8, kWarpMma = 9;
+constexpr int kRows = 128;         // query rows per CTA (= TMEM lanes)
+constexpr int kKeys = 128;         // keys per step
+constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kRegsSoftmax = 216, kRegsOther = 72;  // setmaxnreg split of 384 x 168 registers
+constexpr int kTraceIters = 64, kTraceEv = 16;
+// profiling only (XDIT_TRACE): clock64 stamps of warp 0 / the MMA lane of the first CTA pair
+__device__ __forceinline__ void stamp(const EpiParams& p, int j, int ev) {
+  if (p.trace && j < kTraceIters && blockIdx.x < 2 && (threadIdx.x & 31) == 0)
+    p.trace[(blockIdx.x * kTraceIters + j) * kTraceEv + ev] = clock64();
+}
+
+template <int D>
+struct Cfg {
+  static_assert(D == 128, "CTA-pair kernel: D = 128");
+  static constexpr int kAtom = kRows * 128;         // 128 rows x 128 B (64 bf16 columns)
+  static constexpr int kQBytes = (D / 64) * kAtom;  // this CTA's Q tile
+  static constexpr int kKHalfAtom = 64 * 128;       // 64 keys x 128 B
+  static constexpr int kStageBytes = 16384;         // K half (D/64 atoms of 64 keys) or V half
+  static_assert((D / 64) * kKHalfAtom == kStageBytes && kRows * (D / 2) * 2 == kStageBytes, "stage");
+  static constexpr int kStages = 10;
+  static constexpr int kSmemBar = 512;
+  static constexpr int kSmemBytes = kQBytes + kStages * kStageBytes + kSmemBar + 1024;
+  __host__ __device__ static constexpr uint32_t col_s(int b) { return uint32_t(b) * 128u; }
+  __host__ __device__ static constexpr uint32_t col_p(int b) { return 256u + uint32_t(b) * 64u; }
+  static constexpr uint32_t kColO = 384u;
+  static_assert(kColO + D <= kTmemCols, "TMEM budget");
+};
+
+// Row max of this warp's 64 raw scores (MASK: columns >= valid excluded).
+template <bool MASK>
+__device__ __forceinline__ float max64(const uint32_t (&a)[32], const uint32_t (&bq)[32], int valid) {
+  float m0 = -INFINITY, m1 = -INFINITY, m2 = -INFINITY, m3 = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    float x[4], y[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      x[e] = u2f(a[i + e]);
+      y[e] = u2f(bq[i + e]);
+      if (MASK) {
+        if (i + e >= valid) x[e] = -INFINITY;
+        if (32 + i + e >= valid) y[e] = -INFINITY;
+      }
+    }
+    m0 = fmax3(m0, x[0], x[1]);
+    m1 = fmax3(m1, x[2], x[3]);
+    m2 = fmax3(m2, y[0], y[1]);
+    m3 = fmax3(m3, y[2], y[3]);
+  }
+  return fmax3(m0, m1, fmaxf(m2, m3));
+}
+
+// P = exp2(S * sl2 - m) for 32 of this warp's columns (col0: their first column within the warp's
+// 64, for the ragged-tail mask) into 16 packed bf16x2 registers; returns the fp32 row sum of P.
+// EMU of every 8 column pairs use the FMA-pipe polynomial (exp2_poly2) instead of MUFU.EX2.
+template <bool MASK, int EMU>
+__device__ __forceinline__ float exp_pack32(const uint32_t (&a)[32], int col0, int valid, float sl2,
+                                            float neg_m, uint32_t* pk) {
+  const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(neg_m, neg_m);
+  uint64_t acc0 = pk2(0.f, 0.f), acc1 = acc0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const int col = col0 + 2 * i;
+    const uint64_t x = fma2(pk2(u2f(a[2 * i]), u2f(a[2 * i + 1])), sc2, nm2);
+    float p0, p1;
+    if (!MASK && (i & 7) < EMU) {
+      up2(exp2_poly2(x), p0, p1);
+    } else {
+      float x0, x1;
+      up2(x, x0, x1);
+      p0 = ptx::ex2(x0);
+      p1 = ptx::ex2(x1);
+    }
+    if (MASK) {
+      if (col >= valid) p0 = 0.f;
+      if (col + 1 >= valid) p1 = 0.f;
+    }
+    if (i & 1) acc1 = add2(acc1, pk2(p0, p1));
+    else acc0 = add2(acc0, pk2(p0, p1));
+    pk[i] = ptx::pack_bf16x2(p0, p1);
+  }
+  float s0, s1, s2, s3;
+  up2(acc0, s0, s1);
+  up2(acc1, s2, s3);
+  return (s0 + s1) + (s2 + s3);
+}
+
+template <int D, int EMU>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    attn_fwd_2sm_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
+                        const __grid_constant__ CUtensorMap tmV, const EpiParams p) {
+  using C = Cfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sKV = smem + C::kQBytes;
+  __shared__ float m_pub[2 * kRows];     // [step parity][row]: running max after that step
+  __shared__ float xsum[2 * kRows];      // [warp pair half][row]: partial row sums for the epilogue
+  __shared__ float xref[2 * kRows];      // [warp pair half][row]: the max those sums refer to
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::kStageBytes);
+  uint64_t* q_full = bars;                    // leader: both Q tiles landed
+  uint64_t* kv_full = q_full + 1;             // leader: both halves of a K / V stage landed
+  uint64_t* kv_empty = kv_full + C::kStages;  // each CTA: the pair's MMAs are done with a stage
+  uint64_t* s_full = kv_empty + C::kStages;   // each CTA: S[b] written
+  uint64_t* s_free = s_full + 2;              // leader: the pair's 8 softmax warps of S[b] loaded it
+  uint64_t* p_full = s_free + 2;              // leader: the pair's 8 softmax warps of P[b] stored it
+  uint64_t* pv_done = p_full + 2;             // each CTA: PV reading P[b] completed
+  uint64_t* o_full = pv_done + 2;             // each CTA: last PV completed
+  uint64_t* m_ready = o_full + 1;             // [lane quarter][step parity]: m_pub written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_ready + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = ptx::cluster_ctarank();
+  int item = blockIdx.x >> 1, kv0 = 0, kv_len = p.Skv, piece = -1;
+  if (item >= p.n_full) {  // tail item: one key range of a split (query-tile pair, head, batch)
+    const int r = item - p.n_full;
+    piece = r;
+    item = p.n_full + r / p.n_split;
+    kv0 = (r % p.n_split) * p.kv_chunk;
+    kv_len = min(p.kv_chunk, p.Skv - kv0);
+  }
+  const int hb = item / p.n_qt, h = hb % p.H, b = hb / p.H;
+  const int m0 = (item % p.n_qt) * kRowsPerItem + int(rank) * kRows;  // this CTA's first query row
+  const int n_kv = (kv_len + kKeys - 1) / kKeys;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(q_full, 1);
+    for (int s = 0; s < C::kStages; ++s) {
+      ptx::mbar_init(&kv_full[s], 1);
+      ptx::mbar_init(&kv_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      ptx::mbar_init(&s_full[t], 1);
+      ptx::mbar_init(&s_free[t], 8);  // the 4 warps of step parity t in each CTA
+      ptx::mbar_init(&p_full[t], 8);
+      ptx::mbar_init(&pv_done[t], 1);
+    }
+    ptx::mbar_init(o_full, 1);
+    for (int i = 0; i < 8; ++i) ptx::mbar_init(&m_ready[i], 32);
+    ptx::fence_mbar_init();
+  }
+  if (warp == kWarpMma) {
+    ptx::tmem_alloc_pair(tmem_slot, kTmemCols);
+    ptx::tmem_relinquish_pair();
+  }
+  if (warp == kWarpTma && lane == 0) {
+    ptx::tma_prefetch_desc(&tmQ);
+    ptx::tma_prefetch_desc(&tmK);
+    ptx::tma_prefetch_desc(&tmV);
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated, before any remote use
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 8) {
+   ptx::setmaxnreg_dec<kRegsOther>();
+   if (warp == kWarpTma) {
+    // ===================================================== TMA producer (both CTAs)
+    const uint64_t pol_q = ptx::policy_evict_first();
+    const uint64_t pol_kv = ptx::policy_evict_last();
+    const uint32_t qfull_cl = ptx::mapa(q_full, 0);
+    if (ptx::elect_one()) {
+      if (rank == 0) ptx::mbar_expect_tx(q_full, 2 * C::kQBytes);
+      for (int a = 0; a < D / 64; ++a)
+        ptx::tma_load_4d_pair(sQ + a * C::kAtom, &tmQ, qfull_cl, a * 64, h, m0, b, pol_q);
+    }
+    __syncwarp();
+    for (int it = 0; it < 2 * n_kv; ++it) {
+      const int j = it >> 1, stage = it % C::kStages, round = it / C::kStages;
+      if (round > 0) ptx::mbar_wait_cluster(&kv_empty[stage], (round - 1) & 1);
+      if (ptx::elect_one()) {
+        if (rank == 0) ptx::mbar_expect_tx(&kv_full[stage], 2 * C::kStageBytes);
+        const uint32_t full_cl = ptx::mapa(&kv_full[stage], 0);
+        uint8_t* dst = sKV + stage * C::kStageBytes;
+        if ((it & 1) == 0) {  // K half: keys [64 rank, 64 rank + 64) of the tile, all D columns
+          for (int a = 0; a < D / 64; ++a)
+            ptx::tma_load_4d_pair(dst + a * C::kKHalfAtom, &tmK, full_cl, a * 64, h,
+                                  kv0 + j * kKeys + int(rank) * 64, b, pol_kv);
+        } else {  // V half: all 128 keys, head-dim columns [64 rank, 64 rank + 64)
+          ptx::tma_load_4d_pair(dst, &tmV, full_cl, int(rank) * 64, h, kv0 + j * kKeys, b, pol_kv);
+        }
+      }
+      __syncwarp();
+    }
+   } else if (warp == kWarpMma) {
+    // ===================================================== MMA issuer (leader CTA, one lane)
+    if (rank == 0) {
+      constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(2 * kRows, kKeys, 0, 0);
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(2 * kRows, D, 0, 1);
+      const uint32_t sQa = ptx::smem_u32(sQ), sKVa = ptx::smem_u32(sKV);
+      auto kv_wait = [&](int idx) -> int {
+        const int stage = idx % C::kStages;
+        ptx::mbar_wait_cluster(&kv_full[stage], (idx / C::kStages) & 1);
+        return stage;
+      };
+      // S[jb] = Q K_j^T: A = Q (K-major, 128B swizzle, atoms of 128 rows), B = the K halves
+      // (K-major, atoms of 64 keys); 16-element K step k at atom k/4, byte 32 (k%4).
+      auto qk = [&](int jb, int sK) {
+#pragma unroll
+        for (int k = 0; k < D / 16; ++k)
+          ptx::mma_ss_pair(tmem + C::col_s(jb),
+                           ptx::sdesc_sw128(sQa + (k >> 2) * C::kAtom + (k & 3) * 32, 16, 1024),
+                           ptx::sdesc_sw128(sKVa + sK * C::kStageBytes + (k >> 2) * C::kKHalfAtom + (k & 3) * 32,
+                                            16, 1024),
+                           idesc_qk, k > 0 ? 1u : 0u);
+      };
+      // O += P[jb] V_j: A = P from TMEM, B = the V halves (MN-major: 16-key step k at row 16k).
+      auto pv = [&](int jb, int sV, bool acc) {
+#pragma unroll
+        for (int k = 0; k < kKeys / 16; ++k)
+          ptx::mma_ts_pair(tmem + C::kColO, tmem + C::col_p(jb) + k * 8,
+                           ptx::sdesc_sw128(sKVa + sV * C::kStageBytes + k * 16 * 128, C::kAtom, 1024),
+                           idesc_pv, (acc || k > 0) ? 1u : 0u);
+      };
+      ptx::mbar_wait_cluster(q_full, 0);
+      // QK^T runs two key tiles ahead of PV: S[j%2] is rewritten by QK^T(j+2) as soon as the
+      // softmax has loaded S(j) (it does so in the middle of step j-1), so the tensor core always
+      // has the next score tile queued while PV waits for the softmax.
+      auto issue_qk = [&](int jq) {
+        const int sK = kv_wait(2 * jq);
+        if (jq >= 2) ptx::mbar_wait_cluster(&s_free[jq & 1], ((jq - 2) >> 1) & 1);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          qk(jq & 1, sK);
+          ptx::tc_commit_pair(&s_full[jq & 1]);
+          ptx::tc_commit_pair(&kv_empty[sK]);
+        }
+        __syncwarp();
+      };
+      issue_qk(0);
+      if (n_kv > 1) issue_qk(1);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 2 < n_kv) issue_qk(j + 2);
+        stamp(p, j, 2);
+        const int sV = kv_wait(2 * j + 1);
+        stamp(p, j, 3);
+        ptx::mbar_wait_cluster(&p_full[j & 1], (j >> 1) & 1);
+        stamp(p, j, 4);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          pv(j & 1, sV, j > 0);
+          ptx::tc_commit_pair(&pv_done[j & 1]);
+          ptx::tc_commit_pair(&kv_empty[sV]);
+          if (j == n_kv - 1) ptx::tc_commit_pair(o_full);
+        }
+        __syncwarp();
+        stamp(p, j, 5);
+      }
+    }
+   }
+  } else {
+    ptx::setmaxnreg_inc<kRegsSoftmax>();
+    // ===================================================== softmax (8 warps per CTA)
+    // Warp w owns TMEM lanes / query rows 32 (w%4) .. +31 and the key tiles j = w/4 (mod 2): the two
+    // warps of a lane quarter alternate steps, so one runs its exp2 stream while the other waits
+    // for S, loads it, finds its row max and stores P -- the MUFU pipe of the SM sub-partition
+    // stays busy.  They share the rows' running max m (reading R1: it moves, rescaling O, only when
+    // the tile max exceeds it by more than 2^kRescaleThresh): the warp of step j publishes m(j) in
+    // smem (mbarrier m_ready[w%4][j%2]) right after its max pass, the warp of step j+1 reads it.
+    // Each warp keeps its own partial row sum l_w relative to the m it last used; the epilogue
+    // combines the two.
+    const int g = warp & 3, c = warp >> 2;
+    const int row_in_tile = g * 32 + lane;
+    const uint32_t lane_off = uint32_t(g * 32) << 16;
+    const float sl2 = p.scale_log2;
+    const uint32_t s_free_cl = ptx::mapa(&s_free[c], 0);  // the leader's barriers for S[c] / P[c]
+    const uint32_t p_full_cl = ptx::mapa(&p_full[c], 0);
+    const uint32_t tO = tmem + lane_off + C::kColO;
+    float m_ref = -INFINITY, l = 0.f, m_used = 0.f;
+    for (int j = c; j < n_kv; j += 2) {
+      ptx::mbar_wait_cluster(&s_full[c], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      uint32_t s0[32], s1[32], s2[32], s3[32];
+      const uint32_t tS = tmem + lane_off + C::col_s(c);
+      ptx::tmem_ld32(tS, s0);
+      ptx::tmem_ld32(tS + 32, s1);
+      ptx::tmem_ld32(tS + 64, s2);
+      ptx::tmem_ld32(tS + 96, s3);
+      ptx::tmem_ld_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);  // S[c] may be rewritten by QK^T(j+2)
+      const int valid = kv_len - j * kKeys;  // keys of this tile that exist (C16)
+      const bool ragged = valid < kKeys;
+      const float m_tile = (ragged ? fmaxf(max64<true>(s0, s1, valid), max64<true>(s2, s3, valid - 64))
+                                   : fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64))) * sl2;
+      if (j == 0) {
+        m_used = m_tile;
+      } else {
+        ptx::mbar_wait(&m_ready[g * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+        const float m_prev = m_pub[((j - 1) & 1) * kRows + row_in_tile];
+        const bool up = m_tile > m_prev + kRescaleThresh;
+        m_used = up ? m_tile : m_prev;
+        if (__any_sync(0xffffffffu, up)) {  // rare: O *= 2^(m_prev - m_used) once PV(j-1) is in
+          const float alpha = ptx::ex2(m_prev - m_used);
+          ptx::mbar_wait_cluster(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
+          ptx::tc_fence_after();
+#pragma unroll
+          for (int cc = 0; cc < D; cc += 32) {
+            uint32_t o[32];
+            ptx::tmem_ld32(tO + cc, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+            ptx::tmem_st32(tO + cc, o);
+          }
+          ptx::tmem_st_wait();
+        }
+      }
+      m_pub[(j & 1) * kRows + row_in_tile] = m_used;
+      ptx::mbar_arrive(&m_ready[g * 2 + (j & 1)]);  // all 32 lanes (count 32)
+      if (m_used != m_ref) {
+        l *= ptx::ex2(m_ref - m_used);  // 0 * 0 on this warp's first step
+        m_ref = m_used;
+      }
+      uint32_t pk[32];
+      float rs;
+      if (ragged) {
+        rs = exp_pack32<true, 0>(s0, 0, valid, sl2, -m_used, pk);
+        rs += exp_pack32<true, 0>(s1, 32, valid, sl2, -m_used, pk + 16);
+      } else {
+        rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_used, pk);
+        rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_used, pk + 16);
+      }
+      if (j >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((j - 2) >> 1) & 1);  // P[c] free again
+      ptx::tc_fence_after();
+      const uint32_t tP = tmem + lane_off + C::col_p(c);
+      ptx::tmem_st32(tP, pk);  // keys 0..63
+      if (ragged) {
+        rs += exp_pack32<true, 0>(s2, 64, valid, sl2, -m_used, pk);
+        rs += exp_pack32<true, 0>(s3, 96, valid, sl2, -m_used, pk + 16);
+      } else {
+        rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_used, pk);
+        rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_used, pk + 16);
+      }
+      ptx::tmem_st32(tP + 32, pk);  // keys 64..127
+      l += rs;
+      ptx::tmem_st_wait();
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive_cluster(p_full_cl);
+    }
+    // ------------------------------------------------- epilogue: O / l, LSE
+    // final m = m of the last step; l = sum over both warps of l_w 2^(m_ref_w - m)
+    xsum[c * kRows + row_in_tile] = l;
+    xref[c * kRows + row_in_tile] = m_ref;
+    ptx::named_bar_sync(1 + g, 64);
+    m_used = m_pub[((n_kv - 1) & 1) * kRows + row_in_tile];
+    l = xsum[row_in_tile] * ptx::ex2(xref[row_in_tile] - m_used) +
+        xsum[kRows + row_in_tile] * ptx::ex2(xref[kRows + row_in_tile] - m_used);
+    ptx::mbar_wait_cluster(o_full, 0);
+    ptx::tc_fence_after();
+    const int row = m0 + row_in_tile;
+    const float inv_l = 1.f / l;
+    RowDst dst = rowmap_dst(p.map, b, row, h);
+    void* obase = p.o;
+    float* lbase = p.lse;
+    int of32 = p.out_f32;
+    if (piece >= 0) {  // split tail item: normalised fp32 partial for tail_merge_kernel
+      const int64_t prow = int64_t(piece) * kRowsPerItem + int(rank) * kRows + row_in_tile;
+      const int64_t n_pieces = int64_t(gridDim.x >> 1) - p.n_full;
+      obase = p.part;
+      lbase = p.part + n_pieces * kRowsPerItem * D;
+      of32 = 1;
+      dst.o_off = prow * D;
+      dst.l_off = prow;
+    }
+    const bool valid_row = row < p.Sq;
+#pragma unroll
+    for (int cc = 0; cc < D / 2; cc += 32) {  // this warp writes O columns [c D/2, c D/2 + D/2)
+      const int col = c * (D / 2) + cc;
+      uint32_t o[32];
+      ptx::tmem_ld32(tO + col, o);
+      ptx::tmem_ld_wait();
+      if (valid_row) {
+        if (of32) {
+          float4* dp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + col);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dp[i] = make_float4(u2f(o[4 * i]) * inv_l, u2f(o[4 * i + 1]) * inv_l, u2f(o[4 * i + 2]) * inv_l,
+                                u2f(o[4 * i + 3]) * inv_l);
+        } else {
+          uint4* dp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + col);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dp[i] = make_uint4(ptx::pack_bf16x2(u2f(o[8 * i]) * inv_l, u2f(o[8 * i + 1]) * inv_l),
+                               ptx::pack_bf16x2(u2f(o[8 * i + 2]) * inv_l, u2f(o[8 * i + 3]) * inv_l),
+                               ptx::pack_bf16x2(u2f(o[8 * i + 4]) * inv_l, u2f(o[8 * i + 5]) * inv_l),
+                               ptx::pack_bf16x2(u2f(o[8 * i + 6]) * inv_l, u2f(o[8 * i + 7]) * inv_l));
+        }
+      }
+    }
+    if (c == 0 && valid_row && lbase) lbase[dst.l_off] = (m_used + log2f(l)) * 0.69314718055994530942f;
+  }
+  __syncwarp();
+  ptx::tc_fence_before();
+  ptx::cluster_sync();  // the peer's TMEM / smem stay live until the leader's MMAs are all done
+  ptx::tc_fence_after();
+  if (warp == kWarpMma) ptx::tmem_dealloc_pair(tmem, kTmemCols);
+}
+
+template <int D, int EMU>
+cudaError_t launch_kernel(dim3 grid, const CUtensorMap* m, const EpiParams& p, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(attn_fwd_2sm_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg<D>::kSmemBytes);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  attn_fwd_2sm_kernel<D, EMU><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(m[0], m[1], m[2], p);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+template <int D>
+cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
+  CUtensorMap m[3];
+  if (!make_map(&m[0], a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h, 64, kRows) ||
+      !make_map(&m[1], a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 64, 64) ||
+      !make_map(&m[2], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 64, kKeys))
+    return cudaErrorInvalidValue;
+  EpiParams p{};
+  p.o = a.o;
+  p.lse = a.lse;
+  p.map = a.omap;
+  p.H = a.H;
+  p.Sq = a.Sq;
+  p.Skv = a.Skv;
+  p.out_f32 = a.out_f32;
+  p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  // Work items (256 query rows of one (batch, head)) run one per CTA pair; the last partial wave
+  // of pairs is split over key ranges as in the one-CTA kernel.
+  p.n_qt = (a.Sq + kRowsPerItem - 1) / kRowsPerItem;
+  const int items = p.n_qt * a.H * a.B;
+  p.n_full = items;
+  p.n_split = 1;
+  p.kv_chunk = a.Skv;
+  p.part = nullptr;
+  int n_tail = 0;
+  static const int npairs = [] {
+    int dev = 0, n = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n / 2;
+  }();
+  static const bool no_split = std::getenv("XDIT_NO_TAIL_SPLIT") != nullptr;
+  if (a.scratch && !no_split && items > npairs && items % npairs) {
+    const int rem = items % npairs, n_kv_tiles = (a.Skv + kKeys - 1) / kKeys;
+    int ns = std::min(std::min(npairs / rem, 8), n_kv_tiles / 2);
+    if (ns >= 2) {
+      const int chunk = ((n_kv_tiles + ns - 1) / ns) * kKeys;
+      ns = (a.Skv + chunk - 1) / chunk;
+      const size_t need = size_t(rem) * ns * kRowsPerItem * (D + 1);
+      if (ns >= 2 && need <= a.scratch_floats) {
+        n_tail = rem;
+        p.n_full = items - rem;
+        p.n_split = ns;
+        p.kv_chunk = chunk;
+        p.part = a.scratch;
+      }
+    }
+  }
+  const dim3 grid(2 * (p.n_full + n_tail * p.n_split));
+  static unsigned long long* trace = [] {
+    unsigned long long* t = nullptr;
+    if (std::getenv("XDIT_TRACE")) cudaMalloc(&t, sizeof(unsigned long long) * 2 * kTraceIters * kTraceEv);
+    return t;
+  }();
+  p.trace = trace;
+  if (trace) cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 2 * kTraceIters * kTraceEv, st);
+  static const int emu = [] {
+    const char* e = std::getenv("XDIT_EXP_EMU");
+    return e ? std::atoi(e) : -1;
+  }();
+  cudaError_t err;
+  switch (emu >= 0 ? emu : 2) {
+    case 0: err = launch_kernel<D, 0>(grid, m, p, st); break;
+    case 1: err = launch_kernel<D, 1>(grid, m, p, st); break;
+    case 3: err = launch_kernel<D, 3>(grid, m, p, st); break;
+    default: err = launch_kernel<D, 2>(grid, m, p, st); break;
+  }
+  if (err == cudaSuccess && n_tail) {
+    const int rows = n_tail * kRowsPerItem;
+    tail_merge_kernel<D><<<(rows + 7) / 8, 256, 0, st>>>(p.part, n_tail, p.n_split, p.n_full, p.n_qt, a.H,
+                                                          a.Sq, p);
+    note_launches(1);
+    err = cudaGetLastError();
+  }
+  if (trace) {  // profiling only: stamps of the first pair relative to the leader's first stamp
+    static unsigned long long h[2 * kTraceIters * kTraceEv];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
+    const unsigned long long t0 = h[6];
+    fprintf(stderr, "cta j | kK sfree vwait vK pfull pvdone | e0 e1 ldiss e2 pvd st+land parr decide\n");
+    for (int cta = 0; cta < 2; ++cta)
+      for (int j = 0; j < kTraceIters; ++j) {
+        fprintf(stderr, "%d %d", cta, j);
+        for (int e = 0; e < 14; ++e) {
+          const unsigned long long v = h[(cta * kTraceIters + j) * kTraceEv + e];
+          fprintf(stderr, " %lld", v ? (long long)(v - t0) : -1LL);
+        }
+        fprintf(stderr, "\n");
+      }
+  }
+  return err;
+}
+
+}  // namespace pair2
+}  // namespace
+
+bool attn_fwd_2sm_supports(int D) { return D == 128; }
+
+cudaError_t launch_attn_fwd_2sm(const AttnArgs& a, cudaStream_t st) {
+  if (a.Sq == 0 || a.B == 0) return cudaSuccess;
+  switch (a.D) {
+    case 128: return pair2::launch_d<128>(a, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace xdit

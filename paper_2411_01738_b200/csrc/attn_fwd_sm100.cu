@@ -29,9 +29,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 
-#include "sm100_ptx.cuh"
-#include "xdit_internal.h"
+#include "attn_common.cuh"
 
 namespace xdit {
 namespace {
@@ -71,55 +71,15 @@ struct Cfg {
   __host__ __device__ static constexpr uint32_t col_o(int t) { return 256u + uint32_t(t) * kDp; }
 };
 
-struct EpiParams {
-  void* o;
-  float* lse;
-  xdit_rowmap map;
-  int H, Sq, Skv, out_f32;
-  float scale_log2;
-  // Work decomposition (1-D grid): items are (query-tile pair, head, batch), query tile fastest.
-  // Items [0, n_full) run over all keys; each of the remaining n_tail items is split into n_split
-  // key ranges of kv_chunk keys whose normalised fp32 partials (O, LSE) go to `part` and are merged
-  // by tail_merge_kernel -- this fills the last, partial wave of the grid.
-  int n_qt, n_full, n_split, kv_chunk;
-  float* part;  // [n_tail * n_split][256][D] fp32 O, then [n_tail * n_split][256] fp32 LSE
-  int diag;  // profiling only (XDIT_DIAG): 1 = softmax does no math, 2 = also no MMA<-softmax wait
-  unsigned long long* trace;  // profiling only (XDIT_TRACE): per-iteration clock64 stamps of CTA 0
-};
 
-constexpr int kTraceIters = 64, kTraceEv = 10;
+constexpr int kTraceIters = 64, kTraceEv = 16;
+static_assert(kQTiles * kBlockM == kRowsPerItem, "work item = one query-tile pair");
 __device__ __forceinline__ void stamp(const EpiParams& p, int j, int ev) {
   if (p.trace && j < kTraceIters && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
       (threadIdx.x & 31) == 0)
     p.trace[j * kTraceEv + ev] = clock64();
 }
 
-__device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }
-__device__ __forceinline__ uint32_t f2u(float x) { return __float_as_uint(x); }
-
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t pk2(float lo, float hi) {
-  uint64_t r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-__device__ __forceinline__ void up2(uint64_t v, float& lo, float& hi) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
-}
-__device__ __forceinline__ uint64_t fma2(uint64_t a, uint64_t b, uint64_t c) {
-  uint64_t d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
-  uint64_t d;
-  asm("add.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
 
 // Pass 1 of the softmax of one 128-key tile: the row max of the raw scores S[row, 0:128) read from
 // TMEM (this thread's lane).  MASK: keys >= valid are excluded (ragged KV tail).  Four independent
@@ -151,34 +111,6 @@ __device__ __forceinline__ float row_max(uint32_t tS, int valid) {
   return fmax3(m0, m1, fmaxf(m2, m3));
 }
 
-// exp2 of two packed fp32 values on the FMA pipe (no MUFU): Cody-Waite split x = j + f with
-// j = round(x) (magic-number add), f in [-0.5, 0.5]; 2^f by a degree-4 polynomial with p(0) = 1
-// exactly (minimax on [-0.5, 0.5], max relative error 2.9e-6, mean 3e-7 -- far below the bf16
-// rounding P gets anyway, and no bias on the row sum l); 2^j is added straight into the exponent
-// field.  x is clamped at -125 so the result stays a normal number.
-__device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
-  float x0, x1;
-  up2(x2, x0, x1);
-  x0 = fmaxf(x0, -125.f);
-  x1 = fmaxf(x1, -125.f);
-  const uint64_t xc = pk2(x0, x1);
-  const uint64_t magic = pk2(12582912.f, 12582912.f), nmagic = pk2(-12582912.f, -12582912.f);
-  const uint64_t t = add2(xc, magic);             // 1.5*2^23 + round(x)
-  const uint64_t j = add2(t, nmagic);             // round(x)
-  const uint64_t f = fma2(j, pk2(-1.f, -1.f), xc);  // x - round(x)
-  uint64_t pp = fma2(f, pk2(0.009582849219441414f, 0.009582849219441414f),
-                     pk2(0.055906426161527634f, 0.055906426161527634f));
-  pp = fma2(f, pp, pk2(0.24024099111557007f, 0.24024099111557007f));
-  pp = fma2(f, pp, pk2(0.6931241750717163f, 0.6931241750717163f));
-  pp = fma2(f, pp, pk2(1.f, 1.f));
-  float p0, p1, t0, t1;
-  up2(pp, p0, p1);
-  up2(t, t0, t1);
-  // (bits(t) << 23) == round(x) << 23 (mod 2^32): the magic's own bits shift out
-  const int r0 = __float_as_int(t0) * (1 << 23) + __float_as_int(p0);
-  const int r1 = __float_as_int(t1) * (1 << 23) + __float_as_int(p1);
-  return pk2(__int_as_float(r0), __int_as_float(r1));
-}
 
 // Pass 2: P = exp2(S * scale*log2e - m) for the tile, written back to TMEM as bf16 pairs over the
 // first 64 columns of S (the A operand of the P.V MMA).  Returns the fp32 row sum of P.
@@ -491,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         if (p.diag < 2) ptx::mbar_wait(&p_full[2 * t + 1], jj & 1);
+        if (t == 0) stamp(p, jj, 14);
         ptx::tc_fence_after();
         if (ptx::elect_one()) pv(t, sV, true, 1);
         __syncwarp();
@@ -500,6 +433,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tc_fence_after();
       int sVprev = 0;
       for (int j = 0; j < n_kv; ++j) {
+        stamp(p, j, 13);
         const int sK = kv_wait(2 * j);
         stamp(p, j, 0);
         if (ptx::elect_one()) {
@@ -605,6 +539,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       ptx::tmem_ld32(tS + 64, s1a);
       ptx::tmem_ld32(tS + 96, s1b);
       ptx::tmem_ld_wait();
+      if ((warp & 3) == 0 && lane == 0) stamp(p, j, 9 + 2 * t);
       {
         uint32_t pk[32];
         float rs, mx;
@@ -622,6 +557,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive(&p_full[2 * t]);
+        if ((warp & 3) == 0 && lane == 0) stamp(p, j, 10 + 2 * t);
       }
       {
         uint32_t pk[32];
@@ -718,75 +654,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == kWarpMma) ptx::tmem_dealloc(tmem, kTmemCols);
 }
 
-// Merge of the split tail items (LSE-weighted, as the ring merge a7): one warp per (tail item, row).
-template <int D>
-__global__ void __launch_bounds__(256)
-    tail_merge_kernel(const float* __restrict__ part, int n_tail, int n_split, int n_full, int n_qt,
-                      int H, int Sq, EpiParams p) {
-  const int w = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
-  if (w >= n_tail * (kQTiles * kBlockM)) return;
-  const int ti = w / (kQTiles * kBlockM), rr = w % (kQTiles * kBlockM);
-  const int item = n_full + ti, hb = item / n_qt, h = hb % H, b = hb / H;
-  const int row = (item % n_qt) * (kQTiles * kBlockM) + rr;
-  if (row >= Sq) return;
-  const int64_t n_pieces = int64_t(n_tail) * n_split;
-  const float* plse = part + n_pieces * (kQTiles * kBlockM) * D;
-  float M = -INFINITY;
-  for (int s = 0; s < n_split; ++s) M = fmaxf(M, plse[(int64_t(ti) * n_split + s) * (kQTiles * kBlockM) + rr]);
-  float sum = 0.f;
-  for (int s = 0; s < n_split; ++s) sum += expf(plse[(int64_t(ti) * n_split + s) * (kQTiles * kBlockM) + rr] - M);
-  const float L = M + logf(sum);
-  const RowDst dst = rowmap_dst(p.map, b, row, h);
-  for (int d = lane * 4; d < D; d += 128) {
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < n_split; ++s) {
-      const int64_t pr = (int64_t(ti) * n_split + s) * (kQTiles * kBlockM) + rr;
-      const float wgt = expf(plse[pr] - L);
-      const float4 x = *reinterpret_cast<const float4*>(part + pr * D + d);
-      acc.x += wgt * x.x; acc.y += wgt * x.y; acc.z += wgt * x.z; acc.w += wgt * x.w;
-    }
-    if (p.out_f32) {
-      *reinterpret_cast<float4*>(static_cast<float*>(p.o) + dst.o_off + d) = acc;
-    } else {
-      uint2 v;
-      v.x = ptx::pack_bf16x2(acc.x, acc.y);
-      v.y = ptx::pack_bf16x2(acc.z, acc.w);
-      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.o) + dst.o_off + d) = v;
-    }
-  }
-  if (lane == 0 && p.lse) p.lse[dst.l_off] = L;
-}
 
 // ------------------------------------------------------------------ host side
-PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
-  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-  if (!fn) {
-    cudaDriverEntryPointQueryResult qres;
-    void* ptr = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &qres) ==
-            cudaSuccess &&
-        qres == cudaDriverEntryPointSuccess)
-      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
-  }
-  return fn;
-}
-
-// [B][S][H][D] bf16 view with element strides (sb, ss, sh); box = box_cols columns x 128 rows
-// (64 columns / 128B swizzle, or 16 columns / 32B swizzle for the D=72 tail atom).
-bool make_map(CUtensorMap* map, const void* base, int B, int S, int H, int D, int64_t sb, int64_t ss,
-              int64_t sh, int box_cols = 64) {
-  auto enc = get_encode_fn();
-  if (!enc) return false;
-  cuuint64_t dims[4] = {cuuint64_t(D), cuuint64_t(H), cuuint64_t(S), cuuint64_t(B)};
-  cuuint64_t strides[3] = {cuuint64_t(sh * 2), cuuint64_t(ss * 2), cuuint64_t(sb * 2)};
-  cuuint32_t box[4] = {cuuint32_t(box_cols), 1, 128, 1};
-  cuuint32_t estr[4] = {1, 1, 1, 1};
-  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
-                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS;
-}
 
 template <int D, int EMU>
 cudaError_t launch_kernel(dim3 grid, const CUtensorMap* m, const EpiParams& p, cudaStream_t st) {
@@ -899,10 +768,10 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     cudaStreamSynchronize(st);
     cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
     const unsigned long long t0 = h[0];
-    fprintf(stderr, "j kready qk0iss p1seen p0wait p0seen | s0seen p0arr s1seen p1arr\n");
+    fprintf(stderr, "j kready qk0iss p1seen p0wait p0seen | s0seen p0arr s1seen p1arr | ld0 h0arr ld1 h1arr\n");
     for (int j = 0; j < kTraceIters; ++j) {
       fprintf(stderr, "%d", j);
-      for (int e = 0; e < 9; ++e)
+      for (int e = 0; e < 15; ++e)
         fprintf(stderr, " %lld", h[j * kTraceEv + e] ? (long long)(h[j * kTraceEv + e] - t0) : -1LL);
       fprintf(stderr, "\n");
     }
@@ -921,6 +790,12 @@ size_t attn_scratch_floats(int D) {
 
 cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st) {
   if (a.Sq == 0 || a.B == 0) return cudaSuccess;
+  // XDIT_ATTN_KERNEL=1sm forces the one-CTA kernel where the CTA-pair kernel would run.
+  static const bool force_1sm = [] {
+    const char* e = std::getenv("XDIT_ATTN_KERNEL");
+    return e && std::string(e) == "1sm";
+  }();
+  if (!force_1sm && attn_fwd_2sm_supports(a.D)) return launch_attn_fwd_2sm(a, st);
   switch (a.D) {
     case 64: return launch_d<64>(a, st);
     case 72: return launch_d<72>(a, st);

@@ -33,7 +33,10 @@ struct AttnArgs {
 size_t attn_scratch_floats(int D);
 
 // Launchers return cudaError_t (cudaSuccess on success); argument checks happen in xdit_usp.cpp.
-cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st);  // bf16, D in {64,128}
+cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st);  // bf16, D in {64,72,128}
+// CTA-pair (cta_group::2) variant of the bf16 kernel, used by launch_attn_fwd_sm100 where supported.
+bool attn_fwd_2sm_supports(int D);
+cudaError_t launch_attn_fwd_2sm(const AttnArgs& a, cudaStream_t st);
 cudaError_t launch_attn_fwd_f32(const AttnArgs& a, cudaStream_t st);    // fp32 SIMT, D <= 256
 cudaError_t launch_lse_merge(float* o_acc, float* lse_acc, const float* o_s, const float* lse_s,
                              int B, int S, int Hh, int D, void* fin, float* fin_lse,
