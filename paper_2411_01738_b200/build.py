@@ -54,7 +54,11 @@ def _stale(out, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose_ptxas: bool = False) -> str:
+def build(force: bool = False, verbose_ptxas: bool = False, defines=(), tag: str | None = None) -> str:
+    """Build the library.  `defines`/`tag`: kernel A/B experiments -- extra -D flags, objects in
+    _build_<tag>/ and the library as libxdit_usp_<tag>.so (load it with XDIT_LIB=<path>)."""
+    BUILD = os.path.join(HERE, "_build" + (f"_{tag}" if tag else ""))
+    LIB = os.path.join(HERE, f"libxdit_usp_{tag}.so" if tag else "libxdit_usp.so")
     os.makedirs(BUILD, exist_ok=True)
     inc, lib = nccl_dirs()
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
@@ -67,7 +71,8 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
             continue
         if src.endswith(".cu"):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler",
-                   "-fvisibility=hidden", "-I", INCLUDE, "-I", inc, "-c", src, "-o", obj]
+                   "-fvisibility=hidden", *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", inc, "-c", src,
+                   "-o", obj]
             if verbose_ptxas:
                 cmd.insert(1, "-Xptxas=-v")
         else:
@@ -86,4 +91,7 @@ def build(force: bool = False, verbose_ptxas: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose_ptxas="-v" in sys.argv)
+    args = sys.argv[1:]
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    tag = next((a.split("=", 1)[1] for a in args if a.startswith("--tag=")), None)
+    build(force="--force" in args, verbose_ptxas="-v" in args, defines=defs, tag=tag)

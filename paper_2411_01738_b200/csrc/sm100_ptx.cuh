@@ -41,6 +41,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// Same, with a suspend-time hint: the waiting warp sleeps in hardware until the phase completes
+// (or the hint, in ns, expires) instead of re-polling -- for single-purpose warps (MMA issuer,
+// TMA producer) that share an SM sub-partition with the softmax warps.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra.uni DONE_%=;\n\t"
+      "bra.uni WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
+
 // One lane of a converged warp returns true (elect.sync): the issuing lane for single-thread
 // async instructions (TMA, tcgen05.mma/commit) while the warp stays converged, so operands that
 // all lanes compute identically stay in the uniform datapath.
@@ -289,9 +304,13 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* bar, uint16_t mask = 3)
       "h"(mask)
       : "memory");
 }
-// Named barrier over `nthreads` threads (multiple of 32).
+// Named barrier over `nthreads` threads (multiple of 32).  bar.arrive: signal without waiting
+// (release: the caller's prior shared-memory writes are visible to the threads that sync).
 __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_arrive(uint32_t id, uint32_t nthreads) {
+  asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ------------------------------------------------------------------ register reallocation

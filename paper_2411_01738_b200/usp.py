@@ -11,7 +11,7 @@ import os
 from typing import Optional, Sequence, Tuple
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libxdit_usp.so")
+LIB_PATH = os.environ.get("XDIT_LIB") or os.path.join(HERE, "libxdit_usp.so")  # XDIT_LIB: A/B builds
 
 XDIT_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "DIVISIBILITY", 4: "COMM_MISMATCH",
                5: "EMPTY_SHARD", 6: "ALIGNMENT", 7: "CUDA", 8: "NCCL", 9: "WORKSPACE"}
