@@ -45,6 +45,13 @@ def parse():
     return ap.parse_args()
 
 
+def attn_kernel_name(D: int) -> str:
+    """The bf16 attention kernel the library dispatches for head dim D (attn_fwd_sm100.cu)."""
+    if D == 128 and os.environ.get("XDIT_ATTN_KERNEL") != "1sm":
+        return "attn_fwd_2sm_kernel"
+    return "attn_fwd_sm100_kernel"
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -357,7 +364,7 @@ def main():
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                     "api": "paper_2411_01738_b200.attention (pinned host -> device, result -> host)"},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "tensor", "kernel": "attn_fwd_sm100_kernel", "achieved": kern_tflops,
+            "roofline": {"bound": "tensor", "kernel": attn_kernel_name(w.D), "achieved": kern_tflops,
                          "peak": peak, "unit": "TFLOP/s", "frac": kern_tflops / peak, "traffic": traffic,
                          "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
                          "frac_of_sustained": kern_tflops / peak_sus,

@@ -194,6 +194,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated, before any remote use
+  __syncthreads();      // (also orders the allocator's smem write for tools that model only bar.sync)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
