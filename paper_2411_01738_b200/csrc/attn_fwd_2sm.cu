@@ -3,24 +3,22 @@
 // Same operation as attn_fwd_sm100.cu (§4.1.1 / P:257 §4.1.2;
 // readings C1-C3, C10, R1): O = softmax(Q K^T / sqrt(D)) V and LSE for one (Q block, KV block).
 //
-// Why a second kernel (DESIGN.md §7 "CTA-pair kernel"): in the one-CTA kernel the S_t / P_t TMEM
-// columns alias, so QK^T of the next key tile of a query tile cannot start before the P.V of the
-// current one -- every step of a tile is a serial chain softmax -> PV -> QK^T, and the tensor core
-// idles ~40 % (profiles/r01_ncu_attn_flux.md).  Here the two SMs of a TPC run one 256-row work item
-// together with M = 256 MMAs, which frees TMEM for DOUBLE-BUFFERED S and P per SM:
+// Why a second kernel: in the one-CTA kernel the S_t / P_t TMEM columns alias,
+// so QK^T of the next key tile of a query tile cannot start before the P.V of the current one --
+// every step of a tile is a serial chain softmax -> PV -> QK^T, and the tensor core idles ~40 %
+// (profiles/r01_ncu_attn_flux.md).  Here the two SMs of a TPC run one 256-row work item together
+// with M = 256 MMAs, which frees TMEM for DOUBLE-BUFFERED S and P per SM:
 //   * CTA rank r owns query rows [128 r, 128 r + 128) of the item: its Q tile, its S/P/O in TMEM;
 //   * each CTA loads HALF of every K tile (keys [64 r, 64 r + 64)) and HALF of every V tile
 //     (head-dim columns [64 r, 64 r + 64)): the pair's MMAs read the other half from the peer SM,
 //     so L2->SM traffic per SM equals the one-CTA kernel's (two query tiles per K/V load) and the
 //     smem operand traffic per SM drops to 3/4 (QK^T) and 1/2 (PV);
-//   * the leader's MMA warp issues QK^T(j+1) into S[(j+1)%2] as soon as the softmax has loaded
-//     S(j-1) into registers -- before PV(j) -- so the tensor core always has the next QK^T queued
-//     while the softmax of step j runs; P(j) goes to P[j%2], free once PV(j-2) has completed;
-//   * 8 softmax warps per CTA, two per TMEM lane quarter: warp w handles rows 32 (w%4) .. +31 and
-//     key columns [64 (w/4), 64 (w/4) + 64).  The two halves of a row exchange their tile max
-//     through smem (named barrier per row quarter) and apply the same running max m: it moves --
-//     rescaling O and l -- only when the tile max exceeds it by more than 2^8 (so P <= 2^8 and no
-//     recomputation is ever needed); each half keeps a partial row sum, added in the epilogue.
+//   * the leader's MMA warp issues QK^T(j+2) into S[j%2] as soon as the softmax has loaded S(j)
+//     into registers -- before PV(j) -- so the tensor core has the next score tile queued while the
+//     softmax of step j runs; P(j) goes to P[j%2], free once PV(j-2) has completed;
+//   * 8 softmax warps per CTA, two per TMEM lane quarter, alternating key tiles (see the softmax
+//     section): one runs its exp2 stream while the other loads and reduces its S; they hand the
+//     rows' running max over through smem.
 // TMEM per SM (512 columns): S[0] [0,128) S[1] [128,256) P[0] [256,320) P[1] [320,384) O [384,512).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -476,7 +474,7 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.out_f32 = a.out_f32;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
   // Work items (256 query rows of one (batch, head)) run one per CTA pair; the last partial wave
-  // of pairs is split over key ranges as in the one-CTA kernel.
+  // of pairs is split over key ranges as in the one-CTA kernel (DESIGN.md §7.1 "tail split").
   p.n_qt = (a.Sq + kRowsPerItem - 1) / kRowsPerItem;
   const int items = p.n_qt * a.H * a.B;
   p.n_full = items;
