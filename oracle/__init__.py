@@ -10,6 +10,8 @@ Functions (numpy float64 arrays, layouts as in xdit_oracle.c):
   attention_rows(q, k, v, rows) -> out [B,n,H,D],  lse [B,H,n]       (exact subset of the above)
   shard(S_txt, S_img, N, g)     -> (txt_off, txt_len, img_off, img_len)   (reading C5)
   usp_emulate(q, k, v, S_txt, u, r) -> out, lse                      (readings C5-C9)
+  kv_keep(k, v, S_txt, u, r, g) -> [2,B,H/u,S,D]  KV buffer rank g retains (NEXT 1)
+  cfg_combine(eps_cond, eps_uncond, g) -> eps_uncond + g (eps_cond - eps_uncond)  (NEXT 2)
 """
 from __future__ import annotations
 
@@ -126,3 +128,35 @@ def usp_emulate(q, k, v, S_txt: int, u: int, r: int):
     if rc != 0:
         raise ValueError(f"xo_usp_emulate failed rc={rc}")
     return out, lse
+
+
+def kv_keep(k, v, S_txt: int, u: int, r: int, g: int) -> np.ndarray:
+    """The KV buffer rank g of a USP (Ulysses u x Ring r) group retains after one attention call --
+    SURVEY §8(f) NEXT 1, PAPER P:401-407 ("after communication of K and V in SP-Ulysses and SP-Ring,
+    the intermediate results ... are stored in each device's KV Buffer"; "For SP-Ulysses, we obtain
+    the KV of the sequence within the SP group participating in the computation of the head ... For
+    SP-Ring, we obtain the KV of the sequence within the SP group for all heads").
+
+    Reading (DESIGN.md §3 R2): with USP the rank holds, for its Ulysses head block j = g mod u
+    (heads [j H/u, (j+1) H/u), reading C7), the K and V of EVERY token of the SP group -- the
+    all-to-all gathers its ring block's tokens and the ring rotation brings the other r-1 blocks --
+    laid out [2 (K, V)][B][H/u][S][D] with the sequence in SP-shard order: rank 0's local rows, then
+    rank 1's, ... (each rank's local rows = its text shard then its image shard, reading C5).
+    Index math only: k, v are the global [B, S, H, D] tensors."""
+    k, v = np.asarray(k), np.asarray(v)
+    B, S, H, D = k.shape
+    N, j, Hh = u * r, g % u, H // u
+    rows = np.concatenate([local_rows(S_txt, S - S_txt, N, p) for p in range(N)])
+    out = np.empty((2, B, Hh, S, D), dtype=k.dtype)
+    for t, x in enumerate((k, v)):
+        out[t] = x[:, rows][:, :, j * Hh:(j + 1) * Hh].transpose(0, 2, 1, 3)
+    return out
+
+
+def cfg_combine(eps_cond, eps_uncond, g: float) -> np.ndarray:
+    """Classifier-free-guidance combine of the two CFG branches' noise predictions, computed in fp64
+    -- SURVEY §8(f) NEXT 2 (the two latents are computed separately and gathered
+    after each step; eps_uncond + g (eps_cond - eps_uncond))."""
+    c, u_ = _f64(eps_cond), _f64(eps_uncond)
+    assert c.shape == u_.shape
+    return u_ + float(g) * (c - u_)
