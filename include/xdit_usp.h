@@ -172,6 +172,35 @@ XDIT_API int xdit_usp_attention_f32(const float* q, const float* k, const float*
                            int B, int H, int S_txt, int S_img, int D, int ulysses, int ring,
                            xdit_stream_t stream, xdit_comm_t comm);
 
+/* USP attention that also RETAINS the K,V the rank receives (
+ * DESIGN.md reading R2) -- the KV buffer of hybrid SP + PipeFusion, which "standard SP
+ * implementations ... discard after the Attention computation".  Same contract and result as
+ * xdit_usp_attention (bf16 only), plus:
+ *   kv_keep : DEVICE bf16 [2][B][H/ulysses][S_txt+S_img][D] (K then V), 16-byte aligned, caller
+ *             owned, not NULL (INVALID_ARG).  Filled with the K,V of EVERY token of the SP group for
+ *             this rank's Ulysses head block j = rank % ulysses (heads [j H/u, (j+1) H/u)), the
+ *             sequence in SP-shard order: rank 0's local rows (text shard, then image shard), then
+ *             rank 1's, ...  Ranks sharing a head block end with identical buffers.
+ * Costs one extra HBM copy of each K,V block the rank holds (2 x B x H/u x S x D x 2 bytes). */
+XDIT_API int xdit_usp_attention_kv(const void* q, const void* k, const void* v, void* out, float* lse,
+                                   void* kv_keep, int B, int H, int S_txt, int S_img, int D, int ulysses,
+                                   int ring, xdit_stream_t stream, xdit_comm_t comm);
+
+/* CFG-parallel step tail ("performs an Allgather operation on
+ * the latent space results"; reading R3).
+ * xdit_cfg_combine: out = eps_uncond + g * (eps_cond - eps_uncond) elementwise over n elements,
+ *   computed in fp32 and rounded once (RNE) to dtype (0 bf16, 1 fp32).  All DEVICE buffers, 16-byte
+ *   aligned, n a multiple of 8 (bf16) / 4 (fp32) (ALIGNMENT).  out may alias either input.
+ * xdit_cfg_tail: the same after an NCCL all-gather of each rank's eps_local (n elements) over the
+ *   handle's ranks, which must be exactly the 2 ranks of a cfg pair (COMM_MISMATCH otherwise):
+ *   rank 0 contributes the conditional, rank 1 the unconditional prediction.  eps_gather: DEVICE
+ *   scratch of 2*n elements (receives [eps_cond; eps_uncond]); eps_out receives the combination on
+ *   both ranks.  Stream-ordered on `stream`; errors: INVALID_ARG, ALIGNMENT, NCCL, CUDA. */
+XDIT_API int xdit_cfg_combine(const void* eps_cond, const void* eps_uncond, void* out, int64_t n, float g,
+                              int dtype, xdit_stream_t stream);
+XDIT_API int xdit_cfg_tail(const void* eps_local, void* eps_gather, void* eps_out, int64_t n, float g,
+                           int dtype, xdit_stream_t stream, xdit_comm_t comm);
+
 /* ------------------------------------------------------------------------------------------ */
 /* Stage entry points (single device).  xdit_usp_attention is composed of exactly these          */
 /* launches plus NCCL; they are exported so a single GPU can drive every (ulysses, ring) split   */
@@ -241,6 +270,16 @@ XDIT_API int xdit_uly_unpack(const void* recv, void* y, int B, int Lmax, int Hh,
 XDIT_API int xdit_uly_unpack_out(const void* orecv, const float* lrecv, int64_t peer_stride_bytes,
                         int64_t lse_peer_stride_bytes, void* out, float* lse, int B, int L,
                         int Lmax, int Hh, int D, int u, int elem_bytes, xdit_stream_t stream);
+
+/* KV retention stage: copy a K and a V block [B][S_blk][Hh][D] (element
+ * (b, t, h, d) at base + b*src_b + t*src_s + h*src_h + d) into kv_keep [2][B][Hh][S_total][D]
+ * (K half, then V half) at sequence rows [seq_off, seq_off + S_blk).  xdit_usp_attention_kv calls it
+ * for its ring block after the all-to-all and for every incoming ring block.  16-byte aligned
+ * pointers; D and the strides multiples of 16 bytes / elem_bytes (2 or 4).
+ * Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_kv_retain(const void* k_blk, const void* v_blk, void* kv_keep, int B, int Hh, int S_blk,
+                            int S_total, int seq_off, int D, int64_t src_b, int64_t src_s, int64_t src_h,
+                            int elem_bytes, xdit_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -51,6 +51,12 @@ cudaError_t launch_uly_unpack_out(const void* orecv, const float* lrecv, int64_t
                                   int L, int Lmax, int Hh, int D, int u, int elem_bytes,
                                   cudaStream_t st);
 
+// SURVEY §8(f) NEXT rows (next_ops.cu).
+cudaError_t launch_kv_retain(const void* k, const void* v, void* kv_keep, int B, int Hh, int S_blk, int S_total,
+                             int seq_off, int D, int64_t sb, int64_t ss, int64_t sh, int eb, cudaStream_t st);
+cudaError_t launch_cfg_combine(const void* c, const void* u, void* o, int64_t n, float g, int dtype,
+                               cudaStream_t st);
+
 // Device-side row-map resolution shared by every epilogue that writes through an xdit_rowmap.
 struct RowDst {
   int64_t o_off;  // element offset of (b, row, h, 0)

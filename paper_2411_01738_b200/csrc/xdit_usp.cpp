@@ -261,7 +261,8 @@ int attn_launch(const AttnArgs& a_in, int dtype, cudaStream_t st, const Buf* scr
 
 // One USP attention call; eb = element bytes (2: bf16 / tcgen05 path, 4: fp32 / SIMT path).
 int usp_call(const void* q, const void* k, const void* v, void* out, float* lse, int B, int H,
-             int S_txt, int S_img, int D, int u, int r, cudaStream_t st, xdit_comm_s* c, int eb) {
+             int S_txt, int S_img, int D, int u, int r, cudaStream_t st, xdit_comm_s* c, int eb,
+             void* kv_keep = nullptr) {
   if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
   if (!q || !k || !v || !out) return fail(XDIT_ERR_INVALID_ARG, "q/k/v/out must not be NULL");
   if (u != c->u || r != c->r || u * r != c->nranks)
@@ -274,7 +275,8 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     return fail(XDIT_ERR_UNSUPPORTED, "fp32 path supports D in [1,256], got %d", D);
   if (dtype == 1 && u * r > 1 && (D % 4) != 0)
     return fail(XDIT_ERR_UNSUPPORTED, "fp32 multi-rank path needs D %% 4 == 0, got %d", D);
-  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse))
+  if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse) ||
+      !aligned16(kv_keep))
     return fail(XDIT_ERR_ALIGNMENT, "tensor pointers must be 16-byte aligned");
   if ((int64_t(H) * D * eb) % 16 != 0)
     return fail(XDIT_ERR_ALIGNMENT, "H*D*elem_bytes must be a multiple of 16");
@@ -288,6 +290,13 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
 
   const int i = P.i, Hh = P.Hh, L = P.S_loc[c->rank], Sb = P.S_blk[i];
   const int64_t row = int64_t(Hh) * D;  // elements per (token) row of a head-block tensor
+  // NEXT 1 (reading R2): the KV buffer holds every ring block at its offset in SP-shard order
+  const int S_sp = S_txt + S_img;
+  auto blk_off = [&](int ib) {
+    int o = 0;
+    for (int x = 0; x < ib; ++x) o += P.S_blk[x];
+    return o;
+  };
 
   // ---- N == 1: one kernel straight from the caller's tensors into the caller's output
   if (P.N == 1) {
@@ -297,6 +306,8 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     a.q_b = a.kv_b = int64_t(L) * H * D; a.q_s = a.kv_s = int64_t(H) * D; a.q_h = a.kv_h = D;
     a.omap = plain_map(B, L, H, D);
     a.out_f32 = dtype;
+    if (kv_keep)
+      XCUDA(xdit::launch_kv_retain(k, v, kv_keep, B, H, L, S_sp, 0, D, a.kv_b, a.kv_s, a.kv_h, eb, st));
     return attn_launch(a, dtype, st, &c->tail);
   }
 
@@ -326,6 +337,8 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     q_b = int64_t(Sb) * row;
     q_s = row;
   }
+  if (kv_keep)  // this rank's ring block, right after the all-to-all (or straight from the caller)
+    XCUDA(xdit::launch_kv_retain(Kc, Vc, kv_keep, B, Hh, Sb, S_sp, blk_off(i), D, q_b, q_s, D, eb, st));
 
   // ---- destination of the final O / LSE: the caller's tensors (u == 1) or the reverse-a2a
   //      send buffer, one segment per Ulysses peer (u > 1; reading C15)
@@ -402,6 +415,11 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
         XCUDA(cudaStreamWaitEvent(st, c->ev_recv[s & 1], 0));
         curK = c->kv[nslot][0].p;
         curV = c->kv[nslot][1].p;
+        if (kv_keep) {  // the incoming ring block (index (i - s - 1) mod r) joins the KV buffer
+          const int nsrc = ((src - 1) % P.r + P.r) % P.r;
+          XCUDA(xdit::launch_kv_retain(curK, curV, kv_keep, B, Hh, P.S_blk[nsrc], S_sp, blk_off(nsrc), D,
+                                       int64_t(P.S_blk[nsrc]) * row, row, D, eb, st));
+        }
       }
     }
   }
@@ -430,7 +448,7 @@ extern "C" {
 
 const char* xdit_last_error(void) { return g_err.c_str(); }
 
-int xdit_version(void) { return 100; }
+int xdit_version(void) { return 101; }
 
 uint64_t xdit_launch_count(void) { return xdit::g_launches.load(std::memory_order_relaxed); }
 
@@ -605,6 +623,66 @@ int xdit_usp_attention_f32(const float* q, const float* k, const float* v, float
                            xdit_stream_t stream, xdit_comm_t comm) {
   return usp_call(q, k, v, out, lse, B, H, S_txt, S_img, D, ulysses, ring,
                   reinterpret_cast<cudaStream_t>(stream), comm, 4);
+}
+
+int xdit_usp_attention_kv(const void* q, const void* k, const void* v, void* out, float* lse, void* kv_keep,
+                          int B, int H, int S_txt, int S_img, int D, int ulysses, int ring,
+                          xdit_stream_t stream, xdit_comm_t comm) {
+  if (!kv_keep) return fail(XDIT_ERR_INVALID_ARG, "kv_keep must not be NULL (use xdit_usp_attention)");
+  return usp_call(q, k, v, out, lse, B, H, S_txt, S_img, D, ulysses, ring,
+                  reinterpret_cast<cudaStream_t>(stream), comm, 2, kv_keep);
+}
+
+int xdit_kv_retain(const void* k_blk, const void* v_blk, void* kv_keep, int B, int Hh, int S_blk, int S_total,
+                   int seq_off, int D, int64_t src_b, int64_t src_s, int64_t src_h, int elem_bytes,
+                   xdit_stream_t stream) {
+  if (!k_blk || !v_blk || !kv_keep) return fail(XDIT_ERR_INVALID_ARG, "k_blk, v_blk, kv_keep must not be NULL");
+  if (B < 0 || Hh < 1 || S_blk < 0 || D < 1 || seq_off < 0 || seq_off + S_blk > S_total ||
+      (elem_bytes != 2 && elem_bytes != 4))
+    return fail(XDIT_ERR_INVALID_ARG, "bad kv_retain shape (B=%d Hh=%d S_blk=%d S_total=%d off=%d D=%d eb=%d)", B,
+                Hh, S_blk, S_total, seq_off, D, elem_bytes);
+  const int vec_elems = 16 / elem_bytes;
+  if (!aligned16(k_blk) || !aligned16(v_blk) || !aligned16(kv_keep) || D % vec_elems || src_b % vec_elems ||
+      src_s % vec_elems || src_h % vec_elems)
+    return fail(XDIT_ERR_ALIGNMENT, "kv_retain needs 16-byte aligned pointers, rows and strides");
+  const cudaError_t e = xdit::launch_kv_retain(k_blk, v_blk, kv_keep, B, Hh, S_blk, S_total, seq_off, D, src_b,
+                                               src_s, src_h, elem_bytes, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(XDIT_ERR_CUDA, "kv_retain launch failed: %s", cudaGetErrorString(e));
+  return XDIT_OK;
+}
+
+int xdit_cfg_combine(const void* eps_cond, const void* eps_uncond, void* out, int64_t n, float g, int dtype,
+                     xdit_stream_t stream) {
+  if (!eps_cond || !eps_uncond || !out || n < 0 || (dtype != 0 && dtype != 1))
+    return fail(XDIT_ERR_INVALID_ARG, "cfg_combine: NULL pointer, n < 0 or dtype not in {0,1}");
+  if (!aligned16(eps_cond) || !aligned16(eps_uncond) || !aligned16(out) || n % (dtype == 0 ? 8 : 4))
+    return fail(XDIT_ERR_ALIGNMENT, "cfg_combine needs 16-byte aligned buffers and n %% %d == 0",
+                dtype == 0 ? 8 : 4);
+  const cudaError_t e =
+      xdit::launch_cfg_combine(eps_cond, eps_uncond, out, n, g, dtype, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(XDIT_ERR_CUDA, "cfg_combine launch failed: %s", cudaGetErrorString(e));
+  return XDIT_OK;
+}
+
+int xdit_cfg_tail(const void* eps_local, void* eps_gather, void* eps_out, int64_t n, float g, int dtype,
+                  xdit_stream_t stream, xdit_comm_t comm) {
+  if (!comm) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
+  if (comm->nranks != 2)
+    return fail(XDIT_ERR_COMM_MISMATCH, "cfg_tail needs a handle over exactly the 2 cfg ranks (got %d)",
+                comm->nranks);
+  if (!eps_local || !eps_gather || !eps_out || n < 0 || (dtype != 0 && dtype != 1))
+    return fail(XDIT_ERR_INVALID_ARG, "cfg_tail: NULL pointer, n < 0 or dtype not in {0,1}");
+  const int eb = dtype == 0 ? 2 : 4;
+  if (!aligned16(eps_local) || !aligned16(eps_gather) || !aligned16(eps_out) || n % (dtype == 0 ? 8 : 4))
+    return fail(XDIT_ERR_ALIGNMENT, "cfg_tail needs 16-byte aligned buffers and n %% %d == 0", dtype == 0 ? 8 : 4);
+  XRET(check_async(comm));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  // All-gather of the two branches' predictions over the cfg pair (rank 0 = conditional, rank 1 =
+  // unconditional: reading R3), then the combine on every rank.
+  XNCCL(ncclAllGather(eps_local, eps_gather, size_t(n) * eb, ncclUint8, comm->sp, st));
+  const char* gb = static_cast<const char*>(eps_gather);
+  XCUDA(xdit::launch_cfg_combine(gb, gb + size_t(n) * eb, eps_out, n, g, dtype, st));
+  return XDIT_OK;
 }
 
 int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,

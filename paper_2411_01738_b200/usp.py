@@ -71,6 +71,10 @@ _SIGS = {
     "xdit_comm_destroy": ([_vp], _i),
     "xdit_usp_attention": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
     "xdit_usp_attention_f32": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
+    "xdit_usp_attention_kv": ([_vp] * 6 + [_i] * 7 + [_vp, _vp], _i),
+    "xdit_cfg_combine": ([_vp, _vp, _vp, _i64, ctypes.c_float, _i, _vp], _i),
+    "xdit_cfg_tail": ([_vp, _vp, _vp, _i64, ctypes.c_float, _i, _vp, _vp], _i),
+    "xdit_kv_retain": ([_vp, _vp, _vp] + [_i] * 6 + [_i64] * 3 + [_i, _vp], _i),
     "xdit_attn_fwd": ([_vp] * 5 + [_i] * 5 + [_i64] * 6 + [ctypes.POINTER(RowMap), _i, _i, _vp, ctypes.c_size_t,
                                                             _vp], _i),
     "xdit_attn_scratch_bytes": ([_i], ctypes.c_size_t),
@@ -207,9 +211,11 @@ class Comm:
 
 
 def attention(q, k, v, *, S_txt: int, S_img: int, comm: Comm, ulysses: int = 1, ring: int = 1,
-              out=None, lse=None, return_lse: bool = True, stream=None):
+              out=None, lse=None, return_lse: bool = True, stream=None, kv_keep=None):
     """USP attention of this rank's local tokens: q, k, v [B, S_loc, H, D] (bf16 -> tcgen05 path,
-    fp32 -> SIMT fp32 path).  Returns (out, lse) with lse [B, H, S_loc] fp32 (or None)."""
+    fp32 -> SIMT fp32 path).  Returns (out, lse) with lse [B, H, S_loc] fp32 (or None).
+    kv_keep (bf16 only): a [2, B, H/ulysses, S_txt+S_img, D] bf16 CUDA tensor that receives the
+    K,V of the whole SP group for this rank's heads (xdit_usp_attention_kv)."""
     import torch
     B, L, H, D = q.shape
     for t in (q, k, v):
@@ -221,6 +227,13 @@ def attention(q, k, v, *, S_txt: int, S_img: int, comm: Comm, ulysses: int = 1, 
         lse = torch.empty((B, H, L), dtype=torch.float32, device=q.device)
     f32 = q.dtype == torch.float32
     comm.reserve(B, H, S_txt, S_img, D, 4 if f32 else 2)
+    if kv_keep is not None:
+        if f32:
+            raise XditError(2, "attention", "kv_keep is supported on the bf16 path only")
+        rc = lib().xdit_usp_attention_kv(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(kv_keep), B, H,
+                                         S_txt, S_img, D, ulysses, ring, _stream(stream), comm.handle)
+        _check(rc, "xdit_usp_attention_kv")
+        return out, lse
     fn = lib().xdit_usp_attention_f32 if f32 else lib().xdit_usp_attention
     rc = fn(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), B, H, S_txt, S_img, D, ulysses, ring,
             _stream(stream), comm.handle)
@@ -272,3 +285,42 @@ def uly_unpack_out(orecv_ptr: int, lrecv_ptr: Optional[int], peer_stride_bytes: 
     _check(lib().xdit_uly_unpack_out(orecv_ptr, lrecv_ptr, peer_stride_bytes, lse_peer_stride_bytes,
                                      _ptr(out), _ptr(lse), B, L, Lmax, Hh, D, u, elem_bytes,
                                      _stream(stream)), "xdit_uly_unpack_out")
+
+
+# ------------------------------------------------------------------------- SURVEY §8(f) NEXT rows
+def kv_retain(k_blk, v_blk, kv_keep, *, B: int, Hh: int, S_blk: int, S_total: int, seq_off: int, D: int,
+              strides, stream=None):
+    """Copy a K and a V block ([B][S_blk][Hh][D] with element strides (b, s, h)) into kv_keep
+    [2][B][Hh][S_total][D] at rows [seq_off, seq_off + S_blk) (xdit_kv_retain)."""
+    eb = k_blk.element_size()
+    rc = lib().xdit_kv_retain(_ptr(k_blk), _ptr(v_blk), _ptr(kv_keep), B, Hh, S_blk, S_total, seq_off, D,
+                              int(strides[0]), int(strides[1]), int(strides[2]), eb, _stream(stream))
+    _check(rc, "xdit_kv_retain")
+
+
+def cfg_combine(eps_cond, eps_uncond, g: float, out=None, stream=None):
+    """eps_uncond + g (eps_cond - eps_uncond) on the GPU (fp32 math, one rounding to the dtype)."""
+    import torch
+    if out is None:
+        out = torch.empty_like(eps_cond)
+    dtype = 1 if eps_cond.dtype == torch.float32 else 0
+    rc = lib().xdit_cfg_combine(_ptr(eps_cond), _ptr(eps_uncond), _ptr(out), eps_cond.numel(), float(g), dtype,
+                                _stream(stream))
+    _check(rc, "xdit_cfg_combine")
+    return out
+
+
+def cfg_tail(eps_local, g: float, *, comm: "Comm", gather=None, out=None, stream=None):
+    """CFG step tail over a 2-rank handle: all-gather (rank 0 conditional, rank 1 unconditional),
+    then the combine on every rank (xdit_cfg_tail)."""
+    import torch
+    n = eps_local.numel()
+    if gather is None:
+        gather = torch.empty((2,) + tuple(eps_local.shape), dtype=eps_local.dtype, device=eps_local.device)
+    if out is None:
+        out = torch.empty_like(eps_local)
+    dtype = 1 if eps_local.dtype == torch.float32 else 0
+    rc = lib().xdit_cfg_tail(_ptr(eps_local), _ptr(gather), _ptr(out), n, float(g), dtype, _stream(stream),
+                             comm.handle)
+    _check(rc, "xdit_cfg_tail")
+    return out

@@ -90,3 +90,12 @@ def test_missing_extension_fails_loudly(monkeypatch, tmp_path):
     monkeypatch.setattr(usp, "LIB_PATH", str(tmp_path / "libxdit_usp.so"))
     with pytest.raises(ImportError):
         usp.shard(0, 16, 2, 0)
+
+
+def test_next_rows_reject_bad_arguments_without_gpu():
+    """SURVEY §8(f) NEXT 1-2 entry points validate before touching the device."""
+    L = usp.lib()
+    assert L.xdit_cfg_combine(None, None, None, 8, 1.0, 0, None) == 1  # INVALID_ARG
+    assert L.xdit_cfg_tail(None, None, None, 8, 1.0, 0, None, None) == 1
+    assert L.xdit_kv_retain(None, None, None, 1, 1, 1, 1, 0, 64, 0, 0, 0, 2, None) == 1
+    assert L.xdit_usp_attention_kv(None, None, None, None, None, None, 1, 1, 0, 1, 64, 1, 1, None, None) == 1

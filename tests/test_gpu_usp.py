@@ -106,9 +106,11 @@ def align16(x):
     return (x + 15) // 16 * 16
 
 
-def run_virtual_usp(q, k, v, S_txt, S_img, u, r, f32=False):
+def run_virtual_usp(q, k, v, S_txt, S_img, u, r, f32=False, kv_out=None):
     """Every stage of xdit_usp_attention for all u*r ranks on one GPU; all-to-all and ring P2P are
-    tensor copies between the virtual ranks' buffers.  Returns per-rank (out, lse)."""
+    tensor copies between the virtual ranks' buffers.  Returns per-rank (out, lse).  kv_out (a
+    list): also run xdit_usp_attention_kv's retention stage (xdit_kv_retain after the all-to-all and
+    for every incoming ring block) and append each rank's [2, B, H/u, S, D] KV buffer."""
     B, S, H, D = q.shape
     N = u * r
     eb = 4 if f32 else 2
@@ -146,6 +148,16 @@ def run_virtual_usp(q, k, v, S_txt, S_img, u, r, f32=False):
         else:
             blk = xs[g]
         blocks.append(blk)
+    S_sp = S_txt + S_img
+    blk_off = [sum(plans[x * u].S_blk for x in range(ib)) for ib in range(r)]
+    kvbuf = [torch.full((2, B, Hh, S_sp, D), float("nan"), dtype=dt, device="cuda") for _ in range(N)] \
+        if kv_out is not None else None
+
+    def retain(g, kb, vb, src):
+        Sx = plans[src * u].S_blk
+        st = (Sx * Hh * D, Hh * D, D)
+        usp.kv_retain(kb, vb, kvbuf[g], B=B, Hh=Hh, S_blk=Sx, S_total=S_sp, seq_off=blk_off[src], D=D, strides=st)
+
     # a5-a8: ring loop per rank; final O/LSE written through the rowmap into the reverse-a2a buffer
     ochunk_o = align16(B * Lmax * Hh * D * eb)
     ochunk = ochunk_o + align16(B * Hh * Lmax * 4)
@@ -166,6 +178,8 @@ def run_virtual_usp(q, k, v, S_txt, S_img, u, r, f32=False):
             dst, dst_l = o_final, l_final
             ob = (o_final, l_final)
         qs = (Sb * Hh * D, Hh * D, D)
+        if kvbuf is not None:
+            retain(g, blocks[g][1], blocks[g][2], i)
         if r == 1:
             usp.attn_fwd(qb, blocks[g][1], blocks[g][2], dst, dst_l, B=B, H=Hh, Sq=Sb, Skv=Sb, D=D, q_strides=qs,
                          kv_strides=qs, omap=fmap, dtype=1 if f32 else 0, out_f32=int(f32))
@@ -178,6 +192,8 @@ def run_virtual_usp(q, k, v, S_txt, S_img, u, r, f32=False):
                 src = P.ring_src[s]
                 assert src == (i - s) % r
                 kb, vb = blocks[src * u + j][1], blocks[src * u + j][2]  # block held after s ring steps
+                if kvbuf is not None and s > 0:
+                    retain(g, kb, vb, src)
                 Skv = P.ring_rows[s]
                 ks = (Skv * Hh * D, Hh * D, D)
                 o_s, l_s = (acc_o, acc_l) if s == 0 else (tmp_o, tmp_l)
@@ -208,6 +224,8 @@ def run_virtual_usp(q, k, v, S_txt, S_img, u, r, f32=False):
             assert torch.equal(out[:, :, p * Hh:(p + 1) * Hh], peer), f"rank {g} peer {p}: reverse unpack mismatch"
         outs.append((out, lse))
     torch.cuda.synchronize()
+    if kv_out is not None:
+        kv_out.extend(kvbuf)
     return outs, loc
 
 
@@ -333,3 +351,37 @@ def test_usp_n1_single_token():
     assert torch.equal(out, v)  # one key: O = V exactly
     s = float((q.float() * k.float()).sum()) / 8.0
     assert abs(float(lse[0, 0, 0]) - (float((q[0, 0, 0].float() * k[0, 0, 0].float()).sum()) / 8.0)) < 1e-5
+
+
+# ------------------------------------------------------------------ KV retention
+@pytest.mark.parametrize("u,r", [(2, 1), (1, 2), (2, 2), (4, 2), (2, 4), (1, 8)], ids=lambda x: str(x))
+def test_virtual_usp_kv_retention(u, r):
+    """Every virtual rank's KV buffer equals the oracle's (reading R2) bit for bit, ranks
+    of one head block agree, and the attention result is unchanged."""
+    B, H, S_txt, S_img, D = 2, 8, 33, 400, 64
+    q, k, v = qkv(B, S_txt + S_img, H, D, seed=900 + u * 10 + r)
+    kv = []
+    outs, loc = run_virtual_usp(q, k, v, S_txt, S_img, u, r, kv_out=kv)
+    for g in range(u * r):
+        want = oracle.kv_keep(f64(k), f64(v), S_txt, u, r, g)
+        assert np.array_equal(f64(kv[g]), want), f"rank {g}: retained KV differs from the oracle"
+        assert torch.equal(kv[g], kv[g % u])
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    for g, (o, l) in enumerate(outs):
+        idx = loc[g].numpy()
+        assert_bf16(errors(o, l, ref_o[:, idx], ref_l[:, :, idx]))
+
+
+@pytest.mark.parametrize("S_txt,S_img,D", [(0, 300, 64), (77, 1000, 128), (5, 700, 72)])
+def test_usp_attention_kv_n1(S_txt, S_img, D):
+    """xdit_usp_attention_kv at N = 1 (through the C ABI): same output as xdit_usp_attention and the
+    retained buffer is the head-major K, V (oracle.kv_keep with u = r = 1)."""
+    B, H = 2, 4
+    q, k, v = (t.cuda() for t in qkv(B, S_txt + S_img, H, D, seed=77 + D))
+    buf = torch.full((2, B, H, S_txt + S_img, D), float("nan"), dtype=torch.bfloat16, device="cuda")
+    with usp.Comm(1, 1) as comm:
+        o1, l1 = usp.attention(q, k, v, S_txt=S_txt, S_img=S_img, comm=comm)
+        o2, l2 = usp.attention(q, k, v, S_txt=S_txt, S_img=S_img, comm=comm, kv_keep=buf)
+        torch.cuda.synchronize()
+    assert torch.equal(o1, o2) and torch.equal(l1, l2)
+    assert np.array_equal(f64(buf), oracle.kv_keep(f64(k), f64(v), S_txt, 1, 1, 0))
