@@ -142,7 +142,8 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
 }
 
 // [B][S][H][D] bf16 view with element strides (sb, ss, sh); box = box_cols columns x box_rows rows
-// (64 columns / 128B swizzle, or 16 columns / 32B swizzle for the D=72 tail atom).
+// with the swizzle of the box row: 64 columns / 128B, 32 columns / 64B (the CTA-pair kernel's D=64
+// V halves), 16 columns / 32B (the D=72 tail atom).
 bool make_map(CUtensorMap* map, const void* base, int B, int S, int H, int D, int64_t sb, int64_t ss,
               int64_t sh, int box_cols = 64, int box_rows = 128) {
   auto enc = get_encode_fn();
@@ -153,7 +154,8 @@ bool make_map(CUtensorMap* map, const void* base, int B, int S, int H, int D, in
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides,
                    box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                   box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_32B,
+                   box_cols == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : (box_cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B),
                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

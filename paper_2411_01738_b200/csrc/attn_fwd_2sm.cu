@@ -10,7 +10,7 @@
 // with M = 256 MMAs, which frees TMEM for DOUBLE-BUFFERED S and P per SM:
 //   * CTA rank r owns query rows [128 r, 128 r + 128) of the item: its Q tile, its S/P/O in TMEM;
 //   * each CTA loads HALF of every K tile (keys [64 r, 64 r + 64)) and HALF of every V tile
-//     (head-dim columns [64 r, 64 r + 64)): the pair's MMAs read the other half from the peer SM,
+//     (head-dim columns [D/2 r, D/2 r + D/2)): the pair's MMAs read the other half from the peer SM,
 //     so L2->SM traffic per SM equals the one-CTA kernel's (two query tiles per K/V load) and the
 //     smem operand traffic per SM drops to 3/4 (QK^T) and 1/2 (PV);
 //   * the leader's MMA warp issues QK^T(j+2) into S[j%2] as soon as the softmax has loaded S(j)
@@ -19,7 +19,8 @@
 //   * 8 softmax warps per CTA, two per TMEM lane quarter, alternating key tiles (see the softmax
 //     section): one runs its exp2 stream while the other loads and reduces its S; they hand the
 //     rows' running max over through smem.
-// TMEM per SM (512 columns): S[0] [0,128) S[1] [128,256) P[0] [256,320) P[1] [320,384) O [384,512).
+// TMEM per SM (512 columns): S[0] [0,128) S[1] [128,256) P[0] [256,320) P[1] [320,384) O [384,384+D).
+// Head dims 128 and 64 (the V halves of D = 64 are 32 columns: 64-byte swizzled rows).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -52,13 +53,16 @@ __device__ __forceinline__ void stamp(const EpiParams& p, int j, int ev) {
 
 template <int D>
 struct Cfg {
-  static_assert(D == 128, "CTA-pair kernel: D = 128");
+  static_assert(D == 128 || D == 64, "CTA-pair kernel: D in {64, 128}");
   static constexpr int kAtom = kRows * 128;         // 128 rows x 128 B (64 bf16 columns)
   static constexpr int kQBytes = (D / 64) * kAtom;  // this CTA's Q tile
   static constexpr int kKHalfAtom = 64 * 128;       // 64 keys x 128 B
-  static constexpr int kStageBytes = 16384;         // K half (D/64 atoms of 64 keys) or V half
-  static_assert((D / 64) * kKHalfAtom == kStageBytes && kRows * (D / 2) * 2 == kStageBytes, "stage");
-  static constexpr int kStages = 10;
+  // V half: all 128 keys x D/2 columns; rows of D bytes (128B swizzle at D=128, 64B at D=64)
+  static constexpr int kVRowBytes = D;
+  static constexpr uint32_t kVLayout = D == 128 ? ptx::kLayoutSW128 : ptx::kLayoutSW64;
+  static constexpr int kStageBytes = 128 * D;       // K half (D/64 atoms of 64 keys) or V half
+  static_assert((D / 64) * kKHalfAtom == kStageBytes && kRows * kVRowBytes == kStageBytes, "stage");
+  static constexpr int kStages = D == 128 ? 10 : 20;  // even: K tiles use even stages, V odd
   static constexpr int kSmemBar = 512;
   static constexpr int kSmemBytes = kQBytes + kStages * kStageBytes + kSmemBar + 1024;
   __host__ __device__ static constexpr uint32_t col_s(int b) { return uint32_t(b) * 128u; }
@@ -220,8 +224,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           for (int a = 0; a < D / 64; ++a)
             ptx::tma_load_4d_pair(dst + a * C::kKHalfAtom, &tmK, full_cl, a * 64, h,
                                   kv0 + j * kKeys + int(rank) * 64, b, pol_kv);
-        } else {  // V half: all 128 keys, head-dim columns [64 rank, 64 rank + 64)
-          ptx::tma_load_4d_pair(dst, &tmV, full_cl, int(rank) * 64, h, kv0 + j * kKeys, b, pol_kv);
+        } else {  // V half: all 128 keys, head-dim columns [D/2 rank, D/2 rank + D/2)
+          ptx::tma_load_4d_pair(dst, &tmV, full_cl, int(rank) * (D / 2), h, kv0 + j * kKeys, b, pol_kv);
         }
       }
       __syncwarp();
@@ -253,7 +257,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k)
           ptx::mma_ts_pair(tmem + C::kColO, tmem + C::col_p(jb) + k * 8,
-                           ptx::sdesc_sw128(sKVa + sV * C::kStageBytes + k * 16 * 128, C::kAtom, 1024),
+                           ptx::sdesc(sKVa + sV * C::kStageBytes + k * 16 * C::kVRowBytes, C::kAtom,
+                                      8 * C::kVRowBytes, C::kVLayout),
                            idesc_pv, (acc || k > 0) ? 1u : 0u);
       };
       ptx::mbar_wait_cluster(q_full, 0);
@@ -462,7 +467,7 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   CUtensorMap m[3];
   if (!make_map(&m[0], a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h, 64, kRows) ||
       !make_map(&m[1], a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 64, 64) ||
-      !make_map(&m[2], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 64, kKeys))
+      !make_map(&m[2], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, D / 2, kKeys))
     return cudaErrorInvalidValue;
   EpiParams p{};
   p.o = a.o;
@@ -553,12 +558,13 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
 }  // namespace pair2
 }  // namespace
 
-bool attn_fwd_2sm_supports(int D) { return D == 128; }
+bool attn_fwd_2sm_supports(int D) { return D == 128 || D == 64; }
 
 cudaError_t launch_attn_fwd_2sm(const AttnArgs& a, cudaStream_t st) {
   if (a.Sq == 0 || a.B == 0) return cudaSuccess;
   switch (a.D) {
     case 128: return pair2::launch_d<128>(a, st);
+    case 64: return pair2::launch_d<64>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }
