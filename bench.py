@@ -47,7 +47,7 @@ def parse():
 
 def attn_kernel_name(D: int) -> str:
     """The bf16 attention kernel the library dispatches for head dim D (attn_fwd_sm100.cu)."""
-    if D in (64, 128) and os.environ.get("XDIT_ATTN_KERNEL") != "1sm":
+    if D in (64, 72, 128) and os.environ.get("XDIT_ATTN_KERNEL") != "1sm":
         return "attn_fwd_2sm_kernel"
     return "attn_fwd_sm100_kernel"
 

@@ -53,22 +53,37 @@ __device__ __forceinline__ void stamp(const EpiParams& p, int j, int ev) {
 
 template <int D>
 struct Cfg {
-  static_assert(D == 128 || D == 64, "CTA-pair kernel: D in {64, 128}");
-  static constexpr int kAtom = kRows * 128;         // 128 rows x 128 B (64 bf16 columns)
-  static constexpr int kQBytes = (D / 64) * kAtom;  // this CTA's Q tile
-  static constexpr int kKHalfAtom = 64 * 128;       // 64 keys x 128 B
-  // V half: all 128 keys x D/2 columns; rows of D bytes (128B swizzle at D=128, 64B at D=64)
-  static constexpr int kVRowBytes = D;
+  static_assert(D == 128 || D == 64 || D == 72, "CTA-pair kernel: D in {64, 72, 128}");
+  // Q / K rows (K-major): D/64 atoms of 64 columns with 128-byte swizzle; D = 72 adds one atom of
+  // 16 columns with 32-byte swizzle whose last 8 columns the TMA zero-fills (QK^T K extent 80).
+  static constexpr int kN128 = D / 64;
+  static constexpr bool kTail = (D % 64) != 0;
+  static constexpr int kDpK = kN128 * 64 + (kTail ? 16 : 0);
+  static constexpr int kAtom = kRows * 128, kAtomT = kRows * 32;      // Q atoms (128 rows)
+  static constexpr int kKHalfAtom = 64 * 128, kKHalfAtomT = 64 * 32;  // K-half atoms (64 keys)
+  static constexpr int kQBytes = kN128 * kAtom + (kTail ? kAtomT : 0);
+  static constexpr int kKBytes = kN128 * kKHalfAtom + (kTail ? kKHalfAtomT : 0);
+  // V half (all 128 keys, MN-major): a main atom of kVCols columns per CTA (the pair's PV MMA has
+  // N = 2 kVCols: 64 columns / 128B swizzle at D = 128, 32 columns / 64B swizzle at D = 64, 72)
+  // and, at D = 72, a 16-column 32B-swizzled tail atom per CTA (columns [64 + 16 r, +16) of the
+  // zero-padded 96: the second PV MMA has N = 32 into O columns 64-95).
+  static constexpr int kVCols = D == 128 ? 64 : 32;
+  static constexpr int kVRowBytes = 2 * kVCols;
   static constexpr uint32_t kVLayout = D == 128 ? ptx::kLayoutSW128 : ptx::kLayoutSW64;
-  static constexpr int kStageBytes = 128 * D;       // K half (D/64 atoms of 64 keys) or V half
-  static_assert((D / 64) * kKHalfAtom == kStageBytes && kRows * kVRowBytes == kStageBytes, "stage");
-  static constexpr int kStages = D == 128 ? 10 : 20;  // even: K tiles use even stages, V odd
+  static constexpr int kVBytesA = 128 * kVRowBytes;
+  static constexpr int kVBytes = kVBytesA + (kTail ? 128 * 32 : 0);
+  static constexpr int kNPV = 2 * kVCols;                // N of the main PV MMA
+  static constexpr int kOW = kNPV + (kTail ? 32 : 0);    // O columns in TMEM
+  static constexpr int kStageBytes = ((kKBytes > kVBytes ? kKBytes : kVBytes) + 1023) / 1024 * 1024;
+  static constexpr int kStages = D == 128 ? 10 : (D == 64 ? 20 : 14);  // even: K even stages, V odd
   static constexpr int kSmemBar = 512;
-  static constexpr int kSmemBytes = kQBytes + kStages * kStageBytes + kSmemBar + 1024;
+  static constexpr int kSmemBytes = ((kQBytes + 1023) / 1024 * 1024) + kStages * kStageBytes + kSmemBar + 1024;
+  static constexpr int kQRegion = (kQBytes + 1023) / 1024 * 1024;
   __host__ __device__ static constexpr uint32_t col_s(int b) { return uint32_t(b) * 128u; }
   __host__ __device__ static constexpr uint32_t col_p(int b) { return 256u + uint32_t(b) * 64u; }
   static constexpr uint32_t kColO = 384u;
-  static_assert(kColO + D <= kTmemCols, "TMEM budget");
+  static_assert(kColO + kOW <= kTmemCols, "TMEM budget");
+  static_assert(kSmemBytes <= 227 * 1024, "smem budget");
 };
 
 // Row max of this warp's 64 raw scores (MASK: columns >= valid excluded).
@@ -133,13 +148,15 @@ __device__ __forceinline__ float exp_pack32(const uint32_t (&a)[32], int col0, i
 template <int D, int EMU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_2sm_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
-                        const __grid_constant__ CUtensorMap tmV, const EpiParams p) {
+                        const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmQ16,
+                        const __grid_constant__ CUtensorMap tmK16, const __grid_constant__ CUtensorMap tmV16,
+                        const EpiParams p) {
   using C = Cfg<D>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;
-  uint8_t* sKV = smem + C::kQBytes;
+  uint8_t* sKV = smem + C::kQRegion;
   __shared__ float m_pub[2 * kRows];     // [step parity][row]: running max after that step
   __shared__ float xsum[2 * kRows];      // [warp pair half][row]: partial row sums for the epilogue
   __shared__ float xref[2 * kRows];      // [warp pair half][row]: the max those sums refer to
@@ -193,6 +210,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     ptx::tma_prefetch_desc(&tmQ);
     ptx::tma_prefetch_desc(&tmK);
     ptx::tma_prefetch_desc(&tmV);
+    if (C::kTail) {
+      ptx::tma_prefetch_desc(&tmQ16);
+      ptx::tma_prefetch_desc(&tmK16);
+      ptx::tma_prefetch_desc(&tmV16);
+    }
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated, before any remote use
@@ -209,23 +231,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t qfull_cl = ptx::mapa(q_full, 0);
     if (ptx::elect_one()) {
       if (rank == 0) ptx::mbar_expect_tx(q_full, 2 * C::kQBytes);
-      for (int a = 0; a < D / 64; ++a)
+      for (int a = 0; a < C::kN128; ++a)
         ptx::tma_load_4d_pair(sQ + a * C::kAtom, &tmQ, qfull_cl, a * 64, h, m0, b, pol_q);
+      if (C::kTail)
+        ptx::tma_load_4d_pair(sQ + C::kN128 * C::kAtom, &tmQ16, qfull_cl, C::kN128 * 64, h, m0, b, pol_q);
     }
     __syncwarp();
     for (int it = 0; it < 2 * n_kv; ++it) {
       const int j = it >> 1, stage = it % C::kStages, round = it / C::kStages;
       if (round > 0) ptx::mbar_wait_cluster(&kv_empty[stage], (round - 1) & 1);
       if (ptx::elect_one()) {
-        if (rank == 0) ptx::mbar_expect_tx(&kv_full[stage], 2 * C::kStageBytes);
+        if (rank == 0) ptx::mbar_expect_tx(&kv_full[stage], 2 * ((it & 1) ? C::kVBytes : C::kKBytes));
         const uint32_t full_cl = ptx::mapa(&kv_full[stage], 0);
         uint8_t* dst = sKV + stage * C::kStageBytes;
         if ((it & 1) == 0) {  // K half: keys [64 rank, 64 rank + 64) of the tile, all D columns
-          for (int a = 0; a < D / 64; ++a)
+          for (int a = 0; a < C::kN128; ++a)
             ptx::tma_load_4d_pair(dst + a * C::kKHalfAtom, &tmK, full_cl, a * 64, h,
                                   kv0 + j * kKeys + int(rank) * 64, b, pol_kv);
-        } else {  // V half: all 128 keys, head-dim columns [D/2 rank, D/2 rank + D/2)
-          ptx::tma_load_4d_pair(dst, &tmV, full_cl, int(rank) * (D / 2), h, kv0 + j * kKeys, b, pol_kv);
+          if (C::kTail)
+            ptx::tma_load_4d_pair(dst + C::kN128 * C::kKHalfAtom, &tmK16, full_cl, C::kN128 * 64, h,
+                                  kv0 + j * kKeys + int(rank) * 64, b, pol_kv);
+        } else {  // V half: all 128 keys, head-dim columns [kVCols rank, kVCols rank + kVCols) (+ tail)
+          ptx::tma_load_4d_pair(dst, &tmV, full_cl, int(rank) * C::kVCols, h, kv0 + j * kKeys, b, pol_kv);
+          if (C::kTail)
+            ptx::tma_load_4d_pair(dst + C::kVBytesA, &tmV16, full_cl, 2 * C::kVCols + 16 * int(rank), h,
+                                  kv0 + j * kKeys, b, pol_kv);
         }
       }
       __syncwarp();
@@ -234,7 +264,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================================================== MMA issuer (leader CTA, one lane)
     if (rank == 0) {
       constexpr uint32_t idesc_qk = ptx::idesc_bf16_f32(2 * kRows, kKeys, 0, 0);
-      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(2 * kRows, D, 0, 1);
+      constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(2 * kRows, C::kNPV, 0, 1);
+      constexpr uint32_t idesc_pv16 = ptx::idesc_bf16_f32(2 * kRows, 32, 0, 1);
       const uint32_t sQa = ptx::smem_u32(sQ), sKVa = ptx::smem_u32(sKV);
       auto kv_wait = [&](int idx) -> int {
         const int stage = idx % C::kStages;
@@ -244,22 +275,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       // S[jb] = Q K_j^T: A = Q (K-major, 128B swizzle, atoms of 128 rows), B = the K halves
       // (K-major, atoms of 64 keys); 16-element K step k at atom k/4, byte 32 (k%4).
       auto qk = [&](int jb, int sK) {
+        const uint32_t ka = sKVa + sK * C::kStageBytes;
 #pragma unroll
-        for (int k = 0; k < D / 16; ++k)
-          ptx::mma_ss_pair(tmem + C::col_s(jb),
-                           ptx::sdesc_sw128(sQa + (k >> 2) * C::kAtom + (k & 3) * 32, 16, 1024),
-                           ptx::sdesc_sw128(sKVa + sK * C::kStageBytes + (k >> 2) * C::kKHalfAtom + (k & 3) * 32,
-                                            16, 1024),
-                           idesc_qk, k > 0 ? 1u : 0u);
+        for (int k = 0; k < C::kDpK / 16; ++k) {
+          if (C::kTail && k == C::kN128 * 4)  // D = 72: the 32B-swizzled tail atom is one K step
+            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc(sQa + C::kN128 * C::kAtom, 16, 8 * 32, ptx::kLayoutSW32),
+                             ptx::sdesc(ka + C::kN128 * C::kKHalfAtom, 16, 8 * 32, ptx::kLayoutSW32), idesc_qk,
+                             1u);
+          else
+            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc_sw128(sQa + (k >> 2) * C::kAtom + (k & 3) * 32, 16, 1024),
+                             ptx::sdesc_sw128(ka + (k >> 2) * C::kKHalfAtom + (k & 3) * 32, 16, 1024), idesc_qk,
+                             k > 0 ? 1u : 0u);
+        }
       };
       // O += P[jb] V_j: A = P from TMEM, B = the V halves (MN-major: 16-key step k at row 16k).
       auto pv = [&](int jb, int sV, bool acc) {
+        const uint32_t va = sKVa + sV * C::kStageBytes;
 #pragma unroll
-        for (int k = 0; k < kKeys / 16; ++k)
+        for (int k = 0; k < kKeys / 16; ++k) {
           ptx::mma_ts_pair(tmem + C::kColO, tmem + C::col_p(jb) + k * 8,
-                           ptx::sdesc(sKVa + sV * C::kStageBytes + k * 16 * C::kVRowBytes, C::kAtom,
-                                      8 * C::kVRowBytes, C::kVLayout),
+                           ptx::sdesc(va + k * 16 * C::kVRowBytes, C::kAtom, 8 * C::kVRowBytes, C::kVLayout),
                            idesc_pv, (acc || k > 0) ? 1u : 0u);
+          if (C::kTail)  // D = 72: O columns 64-95 from the 16-column tail atoms of both CTAs
+            ptx::mma_ts_pair(tmem + C::kColO + C::kNPV, tmem + C::col_p(jb) + k * 8,
+                             ptx::sdesc(va + C::kVBytesA + k * 16 * 32, 16, 8 * 32, ptx::kLayoutSW32), idesc_pv16,
+                             (acc || k > 0) ? 1u : 0u);
+        }
       };
       ptx::mbar_wait_cluster(q_full, 0);
       // QK^T runs two key tiles ahead of PV: S[j%2] is rewritten by QK^T(j+2) as soon as the
@@ -345,13 +386,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           ptx::mbar_wait_cluster(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
           ptx::tc_fence_after();
 #pragma unroll
-          for (int cc = 0; cc < D; cc += 32) {
+          for (int cc = 0; cc < (D / 32) * 32; cc += 32) {
             uint32_t o[32];
             ptx::tmem_ld32(tO + cc, o);
             ptx::tmem_ld_wait();
 #pragma unroll
             for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
             ptx::tmem_st32(tO + cc, o);
+          }
+          if (D % 32) {  // D = 72: columns 64-71 (72-95 hold zeros)
+            uint32_t o[8];
+            ptx::tmem_ld8(tO + (D / 32) * 32, o);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+            ptx::tmem_st8(tO + (D / 32) * 32, o);
           }
           ptx::tmem_st_wait();
         }
@@ -416,8 +465,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
     const bool valid_row = row < p.Sq;
 #pragma unroll
-    for (int cc = 0; cc < D / 2; cc += 32) {  // this warp writes O columns [c D/2, c D/2 + D/2)
-      const int col = c * (D / 2) + cc;
+    for (int col = c * 32; col < (D / 32) * 32; col += 64) {  // this warp's 32-column chunks of O
       uint32_t o[32];
       ptx::tmem_ld32(tO + col, o);
       ptx::tmem_ld_wait();
@@ -439,6 +487,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
       }
     }
+    if (D % 32 && c == 0) {  // D = 72: columns 64-71
+      constexpr int col = (D / 32) * 32;
+      uint32_t o[8];
+      ptx::tmem_ld8(tO + col, o);
+      ptx::tmem_ld_wait();
+      if (valid_row) {
+        if (of32) {
+          float4* dp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + col);
+          dp[0] = make_float4(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l, u2f(o[2]) * inv_l, u2f(o[3]) * inv_l);
+          dp[1] = make_float4(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l, u2f(o[6]) * inv_l, u2f(o[7]) * inv_l);
+        } else {
+          uint4* dp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + col);
+          dp[0] = make_uint4(ptx::pack_bf16x2(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l),
+                             ptx::pack_bf16x2(u2f(o[2]) * inv_l, u2f(o[3]) * inv_l),
+                             ptx::pack_bf16x2(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l),
+                             ptx::pack_bf16x2(u2f(o[6]) * inv_l, u2f(o[7]) * inv_l));
+        }
+      }
+    }
     if (c == 0 && valid_row && lbase) lbase[dst.l_off] = (m_used + log2f(l)) * 0.69314718055994530942f;
   }
   __syncwarp();
@@ -457,18 +524,29 @@ cudaError_t launch_kernel(dim3 grid, const CUtensorMap* m, const EpiParams& p, c
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  attn_fwd_2sm_kernel<D, EMU><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(m[0], m[1], m[2], p);
+  attn_fwd_2sm_kernel<D, EMU><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
   note_launches(1);
   return cudaGetLastError();
 }
 
 template <int D>
 cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
-  CUtensorMap m[3];
+  using C = Cfg<D>;
+  CUtensorMap m[6];
   if (!make_map(&m[0], a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h, 64, kRows) ||
       !make_map(&m[1], a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 64, 64) ||
-      !make_map(&m[2], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, D / 2, kKeys))
+      !make_map(&m[2], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, C::kVCols, kKeys))
     return cudaErrorInvalidValue;
+  if (C::kTail) {
+    if (!make_map(&m[3], a.q, a.B, a.Sq, a.H, D, a.q_b, a.q_s, a.q_h, 16, kRows) ||
+        !make_map(&m[4], a.k, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 16, 64) ||
+        !make_map(&m[5], a.v, a.B, a.Skv, a.H, D, a.kv_b, a.kv_s, a.kv_h, 16, kKeys))
+      return cudaErrorInvalidValue;
+  } else {
+    m[3] = m[0];
+    m[4] = m[1];
+    m[5] = m[2];
+  }
   EpiParams p{};
   p.o = a.o;
   p.lse = a.lse;
@@ -558,13 +636,14 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
 }  // namespace pair2
 }  // namespace
 
-bool attn_fwd_2sm_supports(int D) { return D == 128 || D == 64; }
+bool attn_fwd_2sm_supports(int D) { return D == 128 || D == 64 || D == 72; }
 
 cudaError_t launch_attn_fwd_2sm(const AttnArgs& a, cudaStream_t st) {
   if (a.Sq == 0 || a.B == 0) return cudaSuccess;
   switch (a.D) {
     case 128: return pair2::launch_d<128>(a, st);
     case 64: return pair2::launch_d<64>(a, st);
+    case 72: return pair2::launch_d<72>(a, st);
     default: return cudaErrorInvalidValue;
   }
 }
