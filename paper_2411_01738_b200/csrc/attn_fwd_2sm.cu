@@ -360,6 +360,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int j = c; j < n_kv; j += 2) {
       ptx::mbar_wait_cluster(&s_full[c], (j >> 1) & 1);
       ptx::tc_fence_after();
+      if (p.diag) {  // profiling only (XDIT_DIAG=1): hand the barriers back without softmax work
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);
+        if (j >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((j - 2) >> 1) & 1);
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive_cluster(p_full_cl);
+        if (j + 1 < n_kv) {  // keep the running-max hand-over in step
+          if (j > 0) ptx::mbar_wait(&m_ready[g * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
+          m_pub[(j & 1) * kRows + row_in_tile] = 0.f;
+          ptx::mbar_arrive(&m_ready[g * 2 + (j & 1)]);
+        }
+        l = 1.f;
+        m_ref = m_used = 0.f;
+        continue;
+      }
       uint32_t s0[32], s1[32], s2[32], s3[32];
       const uint32_t tS = tmem + lane_off + C::col_s(c);
       ptx::tmem_ld32(tS, s0);
@@ -556,6 +571,11 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.Skv = a.Skv;
   p.out_f32 = a.out_f32;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
+  static const int diag = [] {
+    const char* e = std::getenv("XDIT_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.diag = diag;
   // Work items (256 query rows of one (batch, head)) run one per CTA pair; the last partial wave
   // of pairs is split over key ranges as in the one-CTA kernel (DESIGN.md §7.1 "tail split").
   p.n_qt = (a.Sq + kRowsPerItem - 1) / kRowsPerItem;
