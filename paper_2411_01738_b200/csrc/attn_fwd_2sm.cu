@@ -218,7 +218,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // barriers of both CTAs initialised, TMEM allocated, before any remote use
-  __syncthreads();      // (also orders the allocator's smem write for tools that model only bar.sync)
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -621,7 +620,10 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     return e ? std::atoi(e) : -1;
   }();
   cudaError_t err;
-  switch (emu >= 0 ? emu : 2) {
+  // Default 0: every exp2 on MUFU.  The FMA-pipe polynomial (EMU of 8 column pairs) gained ~1 % in
+  // short runs but draws more power; in the sustained bench the kernel is power-capped and EMU=0
+  // held a higher SM clock (1627 vs 1545 MHz) and throughput (profiles/r01_bench_flux*.json).
+  switch (emu >= 0 ? emu : 0) {
     case 0: err = launch_kernel<D, 0>(grid, m, p, st); break;
     case 1: err = launch_kernel<D, 1>(grid, m, p, st); break;
     case 3: err = launch_kernel<D, 3>(grid, m, p, st); break;
