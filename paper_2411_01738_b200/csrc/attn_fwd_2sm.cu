@@ -86,6 +86,13 @@ struct Cfg {
   static_assert(kSmemBytes <= 227 * 1024, "smem budget");
 };
 
+// Scores of keys >= valid (columns col0.. of this 32-column block) -> -inf: exp2 gives exactly 0.
+__device__ __forceinline__ void mask_tail(uint32_t (&a)[32], int col0, int valid) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    if (col0 + i >= valid) a[i] = f2u(-INFINITY);
+}
+
 // Row max of this warp's 64 raw scores (MASK: columns >= valid excluded).
 template <bool MASK>
 __device__ __forceinline__ float max64(const uint32_t (&a)[32], const uint32_t (&bq)[32], int valid) {
@@ -385,9 +392,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);  // S[c] may be rewritten by QK^T(j+2)
       const int valid = kv_len - j * kKeys;  // keys of this tile that exist (C16)
-      const bool ragged = valid < kKeys;
-      const float m_tile = (ragged ? fmaxf(max64<true>(s0, s1, valid), max64<true>(s2, s3, valid - 64))
-                                   : fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64))) * sl2;
+      if (valid < kKeys) {  // ragged last tile: missing keys get score -inf (weight 0), once, here --
+        // the max and exp code below then has no per-element mask (with the masked variants as
+        // separate template instances the compiler if-converted them into every tile's exp loop)
+        mask_tail(s0, 0, valid);
+        mask_tail(s1, 32, valid);
+        mask_tail(s2, 64, valid);
+        mask_tail(s3, 96, valid);
+      }
+      const float m_tile = fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2;
       if (j == 0) {
         m_used = m_tile;
       } else {
@@ -427,24 +440,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       }
       uint32_t pk[32];
       float rs;
-      if (ragged) {
-        rs = exp_pack32<true, 0>(s0, 0, valid, sl2, -m_used, pk);
-        rs += exp_pack32<true, 0>(s1, 32, valid, sl2, -m_used, pk + 16);
-      } else {
-        rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_used, pk);
-        rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_used, pk + 16);
-      }
+      rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_used, pk);
+      rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_used, pk + 16);
       if (j >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((j - 2) >> 1) & 1);  // P[c] free again
       ptx::tc_fence_after();
       const uint32_t tP = tmem + lane_off + C::col_p(c);
       ptx::tmem_st32(tP, pk);  // keys 0..63
-      if (ragged) {
-        rs += exp_pack32<true, 0>(s2, 64, valid, sl2, -m_used, pk);
-        rs += exp_pack32<true, 0>(s3, 96, valid, sl2, -m_used, pk + 16);
-      } else {
-        rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_used, pk);
-        rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_used, pk + 16);
-      }
+      rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_used, pk);
+      rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_used, pk + 16);
       ptx::tmem_st32(tP + 32, pk);  // keys 64..127
       l += rs;
       ptx::tmem_st_wait();
