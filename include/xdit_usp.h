@@ -55,7 +55,8 @@ typedef enum xdit_status {
   XDIT_ERR_ALIGNMENT = 6,     /* pointer not 16-byte aligned or row bytes not a multiple of 16 */
   XDIT_ERR_CUDA = 7,          /* a CUDA runtime/driver call failed (message has the name) */
   XDIT_ERR_NCCL = 8,          /* an NCCL call failed, or an async NCCL error was pending */
-  XDIT_ERR_WORKSPACE = 9      /* problem exceeds the reservation made by xdit_comm_reserve */
+  XDIT_ERR_WORKSPACE = 9,     /* problem exceeds the reservation made by xdit_comm_reserve */
+  XDIT_ERR_NOT_CONNECTED = 10 /* peer transport: workspace (re)reserved but not (re)connected */
 } xdit_status;
 
 /* Thread-local, NUL-terminated message for the last non-OK return ("" if none).  Valid until the
@@ -105,6 +106,49 @@ XDIT_API int xdit_comm_init(const void* unique_id, int nranks, int rank, int uly
  * framework already owns, NCCL 2.28.x ABI).  The handle does not take ownership of nccl_comm.
  * nccl_comm may be NULL only when ulysses*ring == 1. */
 XDIT_API int xdit_comm_create(void* nccl_comm, int ulysses, int ring, xdit_comm_t* out);
+
+/* ---- Peer-memory transport (no NCCL).  Same mesh and call semantics; the bytes move through
+ * device memory the ranks map into each other (CUDA IPC; NVLink/NVSwitch peer mappings between
+ * GPUs): the Ulysses pack kernel stores each head block straight into the owning peer's receive
+ * buffer (pack + all-to-all in one kernel), ring K/V blocks are copied peer-to-peer into
+ * the next rank's free slot while the attention kernel runs (Table 1 "overlapped"),
+ * and O/LSE chunks are copied back to their token owners.  Streams are ordered across ranks with
+ * 32-bit flags in device memory (cuStreamWriteValue32 into the peer's flag after a system-wide
+ * fence, cuStreamWaitValue32 >= on the local one): nothing spins on an SM and no host thread
+ * waits, so xdit_usp_attention stays stream-ordered and graph-capturable, and several ranks may
+ * share one GPU (one process per rank; ranks in one process are rejected).
+ *
+ * Setup, collective over the SP group (every rank, same order):
+ *   xdit_comm_init_peer -> xdit_comm_reserve -> xdit_comm_peer_export (each rank's blob)
+ *   -> exchange the blobs over any host channel (e.g. torch.distributed all_gather_object)
+ *   -> xdit_comm_peer_connect(all nranks blobs, SP-rank order).
+ * A reserve that reallocates the workspace clears the connection (the call then returns
+ * NOT_CONNECTED) until export/exchange/connect is repeated.  All ranks must have drained their
+ * streams before any rank reserves again or destroys its handle (e.g. synchronize + barrier).
+ * Every rank must issue the same sequence of xdit_usp_attention calls on the handle (each call
+ * advances a per-handle epoch that the flags carry). */
+enum { XDIT_TRANSPORT_NCCL = 0, XDIT_TRANSPORT_PEER = 1 };
+#define XDIT_PEER_BLOB_BYTES 1024
+
+/* Creates a peer-transport handle for SP rank `rank` of nranks = ulysses*ring on the current CUDA
+ * device (no communication).  Errors: INVALID_ARG, COMM_MISMATCH, UNSUPPORTED (the driver has no
+ * stream memory operations), CUDA. */
+XDIT_API int xdit_comm_init_peer(int nranks, int rank, int ulysses, int ring, xdit_comm_t* out);
+
+/* Writes this rank's XDIT_PEER_BLOB_BYTES-byte descriptor (IPC handles of its receive buffers,
+ * ring slots and flag words; HOST memory, caller-owned) to `blob`.  Call after xdit_comm_reserve.
+ * Errors: INVALID_ARG (NULL, or not a peer handle), CUDA. */
+XDIT_API int xdit_comm_peer_export(xdit_comm_t comm, void* blob);
+
+/* Maps the buffers this rank writes into (Ulysses peers' receive buffers, the ring successor's
+ * KV slots, the flag words of both ring neighbours and all Ulysses peers).  `blobs`: HOST array of
+ * nranks descriptors from xdit_comm_peer_export, in SP-rank order.  Replaces any earlier mapping
+ * (device-synchronising).  Errors: INVALID_ARG, COMM_MISMATCH (a blob from another mesh or
+ * position), UNSUPPORTED (two ranks in one process), CUDA (IPC mapping failed). */
+XDIT_API int xdit_comm_peer_connect(xdit_comm_t comm, const void* blobs);
+
+/* XDIT_TRANSPORT_NCCL or XDIT_TRANSPORT_PEER; -1 for NULL. */
+XDIT_API int xdit_comm_transport(xdit_comm_t comm);
 
 /* Allocates (or grows) the device workspace for a problem: Ulysses send/recv buffers, the
  * unpacked Q block, two ring KV slots, fp32 ring accumulators.  Call once per shape before the

@@ -15,10 +15,12 @@ namespace xdit {
 namespace {
 
 template <typename V>
-__global__ void pack_kernel(const V* __restrict__ x, V* __restrict__ send, int B, int L, int Lmax,
-                            int H, int Hh, int vpr /* vectors per (row, head) */, int u, int slot,
-                            int nslots) {
-  // x [B][L][H][vpr] -> send[p][slot][B][Lmax][Hh][vpr], p = h / Hh
+__global__ void pack_kernel(const V* __restrict__ x, PeerDst dst, int B, int L, int Lmax, int H, int Hh,
+                            int vpr /* vectors per (row, head) */, int u, int slot, int nslots) {
+  // x [B][L][H][vpr] -> chunk of Ulysses peer p = h / Hh: dst.p[p] [slot][B][Lmax][Hh][vpr].
+  // dst.p[p] is either this rank's send buffer at chunk p (NCCL transport) or, with the peer-memory
+  // transport, peer p's receive buffer at this rank's chunk -- the stores then travel over NVLink
+  // and the pack IS the all-to-all (one kernel, no staging copy).
   const int64_t n = int64_t(B) * L * H * vpr;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -30,7 +32,7 @@ __global__ void pack_kernel(const V* __restrict__ x, V* __restrict__ send, int B
     const int b = int(r / L);
     const int p = h / Hh, hh = h - p * Hh;
     const int64_t chunk = int64_t(B) * Lmax * Hh * vpr;
-    send[(int64_t(p) * nslots + slot) * chunk + ((int64_t(b) * Lmax + l) * Hh + hh) * vpr + e] = x[i];
+    reinterpret_cast<V*>(dst.p[p])[int64_t(slot) * chunk + ((int64_t(b) * Lmax + l) * Hh + hh) * vpr + e] = x[i];
   }
 }
 
@@ -111,19 +113,29 @@ int vec_bytes(int row_bytes) {
 
 }  // namespace
 
-cudaError_t launch_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u,
-                            int slot, int nslots, int elem_bytes, cudaStream_t st) {
+cudaError_t launch_uly_pack_to(const void* x, const PeerDst& dst, int B, int L, int Lmax, int H, int D, int u,
+                               int slot, int nslots, int elem_bytes, cudaStream_t st) {
   const int rb = D * elem_bytes, vb = vec_bytes(rb), vpr = rb / vb, Hh = H / u;
   const int64_t n = int64_t(B) * L * H * vpr;
   if (n == 0) return cudaSuccess;
   const unsigned g = grid_for(n, 256);
   switch (vb) {
-    case 16: pack_kernel<uint4><<<g, 256, 0, st>>>((const uint4*)x, (uint4*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
-    case 8: pack_kernel<uint2><<<g, 256, 0, st>>>((const uint2*)x, (uint2*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
-    case 4: pack_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)x, (uint32_t*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
-    default: pack_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)x, (uint16_t*)send, B, L, Lmax, H, Hh, vpr, u, slot, nslots); note_launches(1); break;
+    case 16: pack_kernel<uint4><<<g, 256, 0, st>>>((const uint4*)x, dst, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
+    case 8: pack_kernel<uint2><<<g, 256, 0, st>>>((const uint2*)x, dst, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
+    case 4: pack_kernel<uint32_t><<<g, 256, 0, st>>>((const uint32_t*)x, dst, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
+    default: pack_kernel<uint16_t><<<g, 256, 0, st>>>((const uint16_t*)x, dst, B, L, Lmax, H, Hh, vpr, u, slot, nslots); break;
   }
+  note_launches(1);
   return cudaGetLastError();
+}
+
+cudaError_t launch_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u,
+                            int slot, int nslots, int elem_bytes, cudaStream_t st) {
+  // send[p][slot][B][Lmax][H/u][D]: chunk p starts at p * nslots * (B * Lmax * H/u * D) elements
+  PeerDst dst{};
+  const size_t chunk_bytes = size_t(nslots) * B * Lmax * (H / u) * D * elem_bytes;
+  for (int p = 0; p < u && p < 8; ++p) dst.p[p] = static_cast<char*>(send) + p * chunk_bytes;
+  return launch_uly_pack_to(x, dst, B, L, Lmax, H, D, u, slot, nslots, elem_bytes, st);
 }
 
 cudaError_t launch_uly_unpack(const void* recv, void* y, int B, int Lmax, int Hh, int D, int u,

@@ -41,6 +41,12 @@ cudaError_t launch_attn_fwd_f32(const AttnArgs& a, cudaStream_t st);    // fp32 
 cudaError_t launch_lse_merge(float* o_acc, float* lse_acc, const float* o_s, const float* lse_s,
                              int B, int S, int Hh, int D, void* fin, float* fin_lse,
                              const xdit_rowmap* fmap, int fin_dtype, cudaStream_t st);
+// Per-Ulysses-peer destination base addresses of a pack (device pointers, local or peer-mapped).
+struct PeerDst {
+  char* p[8];
+};
+cudaError_t launch_uly_pack_to(const void* x, const PeerDst& dst, int B, int L, int Lmax, int H, int D, int u,
+                               int slot, int nslots, int elem_bytes, cudaStream_t st);
 cudaError_t launch_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u,
                             int slot, int nslots, int elem_bytes, cudaStream_t st);
 cudaError_t launch_uly_unpack(const void* recv, void* y, int B, int Lmax, int Hh, int D, int u,

@@ -6,8 +6,21 @@
 //   Ulysses a2a within the row {i*u + j'} (§4.1.1), Ring P2P within the column {i'*u + j}
 //   (§4.1.1), every collective on an internal high-priority side stream joined back to the
 //   caller's stream with events; no host synchronisation anywhere in the call.
+//
+// Two transports move the bytes:
+//   * NCCL: grouped ncclSend/ncclRecv on the Ulysses / Ring sub-communicators;
+//   * peer memory (xdit_comm_init_peer): every rank maps the receive buffers of the ranks it sends
+//     to (CUDA IPC; over NVLink/NVSwitch between GPUs), the Ulysses pack kernel stores straight
+//     into the peers' receive buffers, ring KV blocks and O chunks are copied peer-to-peer, and the
+//     ranks order their streams with 32-bit flags in device memory -- cuStreamWriteValue32 into the
+//     peer's flag (preceded by a system-wide fence) and cuStreamWaitValue32 (>=) on the local one.
+//     No SM spins and no host thread waits, so the call stays stream-ordered and graph-capturable,
+//     and several ranks may even share one GPU (how the multi-rank tests run on a 1-GPU box).
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -189,8 +202,53 @@ int check_map_align(const xdit_rowmap* m, int vec_elems) {
 
 }  // namespace
 
+namespace {
+// Peer-memory transport: exported buffers (blob handle index) and flag words.
+enum { kHUly = 0, kHORecv = 1, kHKV = 2 /* kHKV + 2*slot + (0 K, 1 V) */, kHFlags = 6, kNHandles = 7 };
+enum { kFA2A = 0, kFO = 8, kFData = 16, kFCredit = 18, kFlagWords = 32 };
+constexpr uint32_t kBlobMagic = 0x31504458u;  // "XDP1"
+struct PeerBlob {
+  uint32_t magic;
+  int32_t rank, nranks, u, r, device, pid;
+  uint32_t valid;                    // bit k: handle k exported
+  uint64_t bytes[kNHandles];         // allocation sizes
+  cudaIpcMemHandle_t h[kNHandles];
+};
+static_assert(sizeof(PeerBlob) <= XDIT_PEER_BLOB_BYTES, "peer blob size");
+
+struct MemOps {
+  PFN_cuStreamWaitValue32_v11070 wait = nullptr;
+  PFN_cuStreamWriteValue32_v11070 write = nullptr;
+};
+const MemOps* memops() {
+  static MemOps m = [] {
+    MemOps x;
+    cudaDriverEntryPointQueryResult q;
+    void* f = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      x.wait = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(f);
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      x.write = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
+    return x;
+  }();
+  return (m.wait && m.write) ? &m : nullptr;
+}
+struct PeerMap {
+  void* ptr[kNHandles] = {};
+  uint64_t bytes[kNHandles] = {};
+  bool opened[kNHandles] = {};  // true: an IPC mapping this handle must close
+};
+}  // namespace
+
 struct xdit_comm_s {
   int nranks = 1, rank = 0, u = 1, r = 1, device = 0;
+  int transport = XDIT_TRANSPORT_NCCL;
+  uint32_t* flags = nullptr;  // peer transport: kFlagWords words written by the peers
+  uint32_t epoch = 0;         // peer transport: calls issued (identical on every rank)
+  bool connected = false;
+  std::vector<PeerMap> peer;  // peer transport: per SP rank (self = local pointers)
   ncclComm_t sp = nullptr, uly = nullptr, ring = nullptr;
   bool own_sp = false;
   cudaStream_t side = nullptr;
@@ -209,7 +267,12 @@ int comm_finish_init(xdit_comm_s* c) {
   cudaEvent_t* evs[] = {&c->ev_start, &c->ev_a2a, &c->ev_o, &c->ev_o_a2a,
                         &c->ev_kdone[0], &c->ev_kdone[1], &c->ev_recv[0], &c->ev_recv[1]};
   for (cudaEvent_t* e : evs) XCUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  if (c->nranks > 1) {
+  if (c->transport == XDIT_TRANSPORT_PEER) {
+    if (!memops()) return fail(XDIT_ERR_UNSUPPORTED, "stream memory operations (cuStreamWaitValue32) unavailable");
+    XCUDA(cudaMalloc(&c->flags, kFlagWords * sizeof(uint32_t)));
+    XCUDA(cudaMemset(c->flags, 0, kFlagWords * sizeof(uint32_t)));
+    XCUDA(cudaDeviceSynchronize());  // zeroed before any peer can map and write them
+  } else if (c->nranks > 1) {
     const int i = c->rank / c->u, j = c->rank % c->u;
     // ncclCommSplit is collective over the SP communicator; every rank takes the same branches.
     if (c->u > 1) XNCCL(ncclCommSplit(c->sp, i, j, &c->uly, nullptr));
@@ -229,6 +292,45 @@ int check_async(xdit_comm_s* c) {
   }
   return XDIT_OK;
 }
+
+// ---- peer-memory transport helpers
+void close_peers(xdit_comm_s* c) {
+  for (PeerMap& m : c->peer)
+    for (int k = 0; k < kNHandles; ++k)
+      if (m.opened[k] && m.ptr[k]) cudaIpcCloseMemHandle(m.ptr[k]);
+  c->peer.clear();
+  c->connected = false;
+}
+
+// Local exported buffers by handle index.
+Buf* exported(xdit_comm_s* c, int k) {
+  switch (k) {
+    case kHUly: return &c->uly_recv;
+    case kHORecv: return &c->orecv;
+    case kHKV + 0: return &c->kv[0][0];
+    case kHKV + 1: return &c->kv[0][1];
+    case kHKV + 2: return &c->kv[1][0];
+    case kHKV + 3: return &c->kv[1][1];
+    default: return nullptr;
+  }
+}
+
+// Stream-ordered signal: *peer_flag = v after all prior work of `st` (system-wide fence first).
+int post_flag(cudaStream_t st, uint32_t* peer_flag, uint32_t v) {
+  const CUresult r = memops()->write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(peer_flag), v,
+                                     CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) return fail(XDIT_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
+  return XDIT_OK;
+}
+// Stream-ordered wait: later work of `st` starts once (int32)(*flag - v) >= 0.
+int wait_flag(cudaStream_t st, const uint32_t* flag, uint32_t v) {
+  const CUresult r = memops()->wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
+                                    CU_STREAM_WAIT_VALUE_GEQ);
+  if (r != CUDA_SUCCESS) return fail(XDIT_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", int(r));
+  return XDIT_OK;
+}
+// Ring step counter of the peer transport: epoch e, step s < 8.
+inline uint32_t ring_t(uint32_t e, int s) { return e * 8u + uint32_t(s); }
 
 // Byte-exact all-to-all of `chunk` bytes per peer on `comm` (send[p] -> peer p -> recv[p]).
 int a2a(ncclComm_t comm, int n, const void* send, void* recv, size_t chunk, cudaStream_t st) {
@@ -283,10 +385,30 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
   Plan P;
   XRET(make_plan(B, H, S_txt, S_img, D, u, r, c->rank, &P));
   const Sizes need = sizes_for(P, B, D, eb);
-  if (need.uly3 > c->uly_send.bytes || need.qblk > c->qblk.bytes || need.kvslot > c->kv[1][0].bytes ||
+  if (need.uly3 > c->uly_recv.bytes || need.qblk > c->qblk.bytes || need.kvslot > c->kv[1][0].bytes ||
       need.oacc > c->oacc.bytes || need.lacc > c->lacc.bytes || need.ochunk * P.u > c->osend.bytes * (P.u > 1))
     return fail(XDIT_ERR_WORKSPACE, "problem exceeds the reservation; call xdit_comm_reserve first");
   XRET(check_async(c));
+  const bool peer = c->transport == XDIT_TRANSPORT_PEER && P.N > 1;
+  if (peer) {
+    if (!c->connected)
+      return fail(XDIT_ERR_NOT_CONNECTED, "peer transport: call xdit_comm_peer_connect after xdit_comm_reserve");
+    for (int q = 0; q < P.N; ++q) {  // buffers this rank writes into on peer q
+      const PeerMap& m = c->peer[q];
+      const bool uly_peer = q / P.u == P.i && P.u > 1, ring_next = q == ((P.i + 1) % P.r) * P.u + P.j && P.r > 1;
+      bool ok = !(uly_peer || ring_next) || m.ptr[kHFlags];
+      if (uly_peer) ok = ok && m.bytes[kHUly] >= need.uly3 && m.bytes[kHORecv] >= need.ochunk * P.u;
+      if (ring_next)
+        for (int k = 0; k < 4; ++k) ok = ok && m.bytes[kHKV + k] >= need.kvslot;
+      if (!ok)
+        return fail(XDIT_ERR_WORKSPACE,
+                    "peer %d's mapped workspace is smaller than this problem (flags %p, uly %llu/%zu, orecv %llu/%zu, "
+                    "kv %llu/%zu)", q, m.ptr[kHFlags], (unsigned long long)m.bytes[kHUly], need.uly3,
+                    (unsigned long long)m.bytes[kHORecv], need.ochunk * P.u, (unsigned long long)m.bytes[kHKV],
+                    need.kvslot);
+    }
+  }
+  const uint32_t e = peer ? ++c->epoch : 0u;  // every rank issues the same calls: epochs agree
 
   const int i = P.i, Hh = P.Hh, L = P.S_loc[c->rank], Sb = P.S_blk[i];
   const int64_t row = int64_t(Hh) * D;  // elements per (token) row of a head-block tensor
@@ -319,13 +441,27 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
   int64_t q_b = int64_t(L) * H * D, q_s = int64_t(H) * D;
   if (P.u > 1) {
     const void* src[3] = {q, k, v};
-    for (int t = 0; t < 3; ++t)
-      XCUDA(xdit::launch_uly_pack(src[t], c->uly_send.p, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
-    XCUDA(cudaEventRecord(c->ev_a2a, st));
-    XCUDA(cudaStreamWaitEvent(c->side, c->ev_a2a, 0));
-    XRET(a2a(c->uly, P.u, c->uly_send.p, c->uly_recv.p, need.uly3 / P.u, c->side));
-    XCUDA(cudaEventRecord(c->ev_a2a, c->side));
-    XCUDA(cudaStreamWaitEvent(st, c->ev_a2a, 0));
+    if (peer) {
+      // pack = all-to-all: head block p of every local token is stored straight into Ulysses peer
+      // p's receive buffer at this rank's chunk (P.j); then flag each peer and wait for theirs.
+      xdit::PeerDst pd{};
+      for (int p = 0; p < P.u; ++p)
+        pd.p[p] = static_cast<char*>(c->peer[i * P.u + p].ptr[kHUly]) + size_t(P.j) * (need.uly3 / P.u);
+      for (int t = 0; t < 3; ++t)
+        XCUDA(xdit::launch_uly_pack_to(src[t], pd, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
+      for (int p = 0; p < P.u; ++p)
+        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFA2A + P.j, e));
+      for (int p = 0; p < P.u; ++p)
+        if (p != P.j) XRET(wait_flag(st, c->flags + kFA2A + p, e));
+    } else {
+      for (int t = 0; t < 3; ++t)
+        XCUDA(xdit::launch_uly_pack(src[t], c->uly_send.p, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
+      XCUDA(cudaEventRecord(c->ev_a2a, st));
+      XCUDA(cudaStreamWaitEvent(c->side, c->ev_a2a, 0));
+      XRET(a2a(c->uly, P.u, c->uly_send.p, c->uly_recv.p, need.uly3 / P.u, c->side));
+      XCUDA(cudaEventRecord(c->ev_a2a, c->side));
+      XCUDA(cudaStreamWaitEvent(st, c->ev_a2a, 0));
+    }
     int len[8] = {0};
     for (int p = 0; p < P.u; ++p) len[p] = P.S_loc[i * P.u + p];
     XCUDA(xdit::launch_uly_unpack(c->uly_recv.p, c->qblk.p, B, P.Lmax, Hh, D, P.u, len, 0, 3, eb, st));
@@ -373,6 +509,14 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
   } else {
     // ---- a5-a7: ring loop; step s attends to the KV block of ring index (i - s) mod r (C9)
     const int nxt_peer = (i + 1) % P.r, prv_peer = (i - 1 + P.r) % P.r;
+    // peer transport: the ring neighbours' SP ranks, and slot-credit protocol.  Rank i pushes its
+    // current block into next's slot (s+1)&1 once next has posted that it finished reading that
+    // slot (credit = ring_t of its last read + 1): step s-1 of this call, or for s = 0 the last odd
+    // step of the previous call.  It posts its own credit for slot s&1 to prev after attention
+    // step s and after its own push out of that slot; next waits for data = ring_t(e, s) + 1.
+    const PeerMap* pnext = peer ? &c->peer[nxt_peer * P.u + P.j] : nullptr;
+    const PeerMap* pprev = peer ? &c->peer[prv_peer * P.u + P.j] : nullptr;
+    const int last_odd = ((P.r - 1) & 1) ? P.r - 1 : P.r - 2;  // r >= 2
     const void* curK = Kc;
     const void* curV = Vc;
     xdit_rowmap accmap = plain_map(B, Sb, Hh, D);
@@ -386,12 +530,21 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
         XCUDA(cudaStreamWaitEvent(c->side, c->ev_start, 0));
         const int nsrc = ((src - 1) % P.r + P.r) % P.r;
         const size_t sbytes = size_t(B) * Skv * row * eb, rbytes = size_t(B) * P.S_blk[nsrc] * row * eb;
-        XNCCL(ncclGroupStart());
-        XNCCL(ncclSend(curK, sbytes, ncclUint8, nxt_peer, c->ring, c->side));
-        XNCCL(ncclSend(curV, sbytes, ncclUint8, nxt_peer, c->ring, c->side));
-        XNCCL(ncclRecv(c->kv[nslot][0].p, rbytes, ncclUint8, prv_peer, c->ring, c->side));
-        XNCCL(ncclRecv(c->kv[nslot][1].p, rbytes, ncclUint8, prv_peer, c->ring, c->side));
-        XNCCL(ncclGroupEnd());
+        if (peer) {
+          const uint32_t credit = s >= 1 ? ring_t(e, s - 1) + 1 : (e > 1 ? ring_t(e - 1, last_odd) + 1 : 0u);
+          XRET(wait_flag(c->side, c->flags + kFCredit + nslot, credit));
+          XCUDA(cudaMemcpyAsync(pnext->ptr[kHKV + 2 * nslot], curK, sbytes, cudaMemcpyDefault, c->side));
+          XCUDA(cudaMemcpyAsync(pnext->ptr[kHKV + 2 * nslot + 1], curV, sbytes, cudaMemcpyDefault, c->side));
+          XRET(post_flag(c->side, static_cast<uint32_t*>(pnext->ptr[kHFlags]) + kFData + nslot, ring_t(e, s) + 1));
+          (void)rbytes;
+        } else {
+          XNCCL(ncclGroupStart());
+          XNCCL(ncclSend(curK, sbytes, ncclUint8, nxt_peer, c->ring, c->side));
+          XNCCL(ncclSend(curV, sbytes, ncclUint8, nxt_peer, c->ring, c->side));
+          XNCCL(ncclRecv(c->kv[nslot][0].p, rbytes, ncclUint8, prv_peer, c->ring, c->side));
+          XNCCL(ncclRecv(c->kv[nslot][1].p, rbytes, ncclUint8, prv_peer, c->ring, c->side));
+          XNCCL(ncclGroupEnd());
+        }
         XCUDA(cudaEventRecord(c->ev_recv[s & 1], c->side));
       }
       a.k = curK; a.v = curV; a.Skv = Skv;
@@ -412,7 +565,11 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
                                      dtype == 0 ? 0 : 1, st));
       }
       if (s < P.r - 1) {
-        XCUDA(cudaStreamWaitEvent(st, c->ev_recv[s & 1], 0));
+        XCUDA(cudaStreamWaitEvent(st, c->ev_recv[s & 1], 0));  // (peer: my push out of this block is done)
+        if (peer) {
+          XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), ring_t(e, s) + 1));
+          XRET(wait_flag(st, c->flags + kFData + nslot, ring_t(e, s) + 1));
+        }
         curK = c->kv[nslot][0].p;
         curV = c->kv[nslot][1].p;
         if (kv_keep) {  // the incoming ring block (index (i - s - 1) mod r) joins the KV buffer
@@ -420,17 +577,30 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
           XCUDA(xdit::launch_kv_retain(curK, curV, kv_keep, B, Hh, P.S_blk[nsrc], S_sp, blk_off(nsrc), D,
                                        int64_t(P.S_blk[nsrc]) * row, row, D, eb, st));
         }
+      } else if (peer) {  // last step: its slot's credit (read by prev's next call when s is odd)
+        XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), ring_t(e, s) + 1));
       }
     }
   }
 
   // ---- a9-a10: reverse all-to-all of O (+ LSE) and unpack into the caller's layout
   if (P.u > 1) {
-    XCUDA(cudaEventRecord(c->ev_o, st));
-    XCUDA(cudaStreamWaitEvent(c->side, c->ev_o, 0));
-    XRET(a2a(c->uly, P.u, c->osend.p, c->orecv.p, need.ochunk, c->side));
-    XCUDA(cudaEventRecord(c->ev_o_a2a, c->side));
-    XCUDA(cudaStreamWaitEvent(st, c->ev_o_a2a, 0));
+    if (peer) {  // chunk p (O rows + LSE of peer p's tokens) -> peer p's receive buffer at chunk P.j
+      for (int p = 0; p < P.u; ++p)
+        XCUDA(cudaMemcpyAsync(static_cast<char*>(c->peer[i * P.u + p].ptr[kHORecv]) + size_t(P.j) * need.ochunk,
+                              static_cast<const char*>(c->osend.p) + size_t(p) * need.ochunk, need.ochunk,
+                              cudaMemcpyDefault, st));
+      for (int p = 0; p < P.u; ++p)
+        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFO + P.j, e));
+      for (int p = 0; p < P.u; ++p)
+        if (p != P.j) XRET(wait_flag(st, c->flags + kFO + p, e));
+    } else {
+      XCUDA(cudaEventRecord(c->ev_o, st));
+      XCUDA(cudaStreamWaitEvent(c->side, c->ev_o, 0));
+      XRET(a2a(c->uly, P.u, c->osend.p, c->orecv.p, need.ochunk, c->side));
+      XCUDA(cudaEventRecord(c->ev_o_a2a, c->side));
+      XCUDA(cudaStreamWaitEvent(st, c->ev_o_a2a, 0));
+    }
     XCUDA(xdit::launch_uly_unpack_out(
         c->orecv.p,
         reinterpret_cast<const float*>(static_cast<const char*>(c->orecv.p) + need.ochunk_o),
@@ -562,13 +732,103 @@ int xdit_comm_create(void* nccl_comm, int ulysses, int ring, xdit_comm_t* out) {
   return XDIT_OK;
 }
 
+int xdit_comm_init_peer(int nranks, int rank, int ulysses, int ring, xdit_comm_t* out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks || ulysses < 1 || ring < 1)
+    return fail(XDIT_ERR_INVALID_ARG, "xdit_comm_init_peer: bad arguments");
+  if (ulysses * ring != nranks)
+    return fail(XDIT_ERR_COMM_MISMATCH, "ulysses*ring=%d != nranks=%d", ulysses * ring, nranks);
+  auto* c = new xdit_comm_s();
+  c->nranks = nranks;
+  c->rank = rank;
+  c->u = ulysses;
+  c->r = ring;
+  c->transport = XDIT_TRANSPORT_PEER;
+  int rc = comm_finish_init(c);
+  if (rc != XDIT_OK) {
+    xdit_comm_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return XDIT_OK;
+}
+
+int xdit_comm_transport(xdit_comm_t c) { return c ? c->transport : -1; }
+
+int xdit_comm_peer_export(xdit_comm_t c, void* blob) {
+  if (!c || !blob) return fail(XDIT_ERR_INVALID_ARG, "xdit_comm_peer_export: NULL argument");
+  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
+  PeerBlob b{};
+  b.magic = kBlobMagic;
+  b.rank = c->rank;
+  b.nranks = c->nranks;
+  b.u = c->u;
+  b.r = c->r;
+  b.device = c->device;
+  b.pid = int32_t(getpid());
+  for (int k = 0; k < kNHandles; ++k) {
+    void* p = k == kHFlags ? static_cast<void*>(c->flags) : exported(c, k)->p;
+    if (!p) continue;
+    XCUDA(cudaIpcGetMemHandle(&b.h[k], p));
+    b.bytes[k] = k == kHFlags ? kFlagWords * sizeof(uint32_t) : exported(c, k)->bytes;
+    b.valid |= 1u << k;
+  }
+  std::memset(blob, 0, XDIT_PEER_BLOB_BYTES);
+  std::memcpy(blob, &b, sizeof b);
+  return XDIT_OK;
+}
+
+int xdit_comm_peer_connect(xdit_comm_t c, const void* blobs) {
+  if (!c || !blobs) return fail(XDIT_ERR_INVALID_ARG, "xdit_comm_peer_connect: NULL argument");
+  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
+  std::vector<PeerBlob> bl(c->nranks);
+  for (int q = 0; q < c->nranks; ++q) {
+    std::memcpy(&bl[q], static_cast<const char*>(blobs) + size_t(q) * XDIT_PEER_BLOB_BYTES, sizeof(PeerBlob));
+    const PeerBlob& b = bl[q];
+    if (b.magic != kBlobMagic || b.rank != q || b.nranks != c->nranks || b.u != c->u || b.r != c->r)
+      return fail(XDIT_ERR_COMM_MISMATCH, "peer blob %d is not rank %d of this (%d x %d) mesh", q, q, c->u, c->r);
+    if (q != c->rank && b.pid == int32_t(getpid()))
+      return fail(XDIT_ERR_UNSUPPORTED, "ranks %d and %d live in one process (one process per rank)", q, c->rank);
+  }
+  XCUDA(cudaDeviceSynchronize());
+  close_peers(c);
+  c->peer.assign(c->nranks, PeerMap{});
+  const int i = c->rank / c->u, j = c->rank % c->u;
+  const int nxt = ((i + 1) % c->r) * c->u + j, prv = ((i - 1 + c->r) % c->r) * c->u + j;
+  for (int q = 0; q < c->nranks; ++q) {
+    PeerMap& m = c->peer[q];
+    const bool uly_peer = q / c->u == i && c->u > 1, ring_nb = c->r > 1 && (q == nxt || q == prv);
+    for (int k = 0; k < kNHandles; ++k) {
+      const bool want = k == kHFlags ? (uly_peer || ring_nb)
+                                     : (k < kHKV ? uly_peer : (c->r > 1 && q == nxt));
+      if (!want || !(bl[q].valid & (1u << k))) continue;
+      m.bytes[k] = bl[q].bytes[k];
+      if (q == c->rank) {
+        m.ptr[k] = k == kHFlags ? static_cast<void*>(c->flags) : exported(c, k)->p;
+        continue;
+      }
+      cudaError_t e = cudaIpcOpenMemHandle(&m.ptr[k], bl[q].h[k], cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) {
+        m.ptr[k] = nullptr;
+        close_peers(c);
+        return fail(XDIT_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d, buffer %d): %s", q, k, cudaGetErrorString(e));
+      }
+      m.opened[k] = true;
+    }
+  }
+  c->connected = true;
+  return XDIT_OK;
+}
+
 int xdit_comm_reserve(xdit_comm_t c, int B, int H, int S_txt, int S_img, int D, int elem_bytes) {
   if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
   if (elem_bytes != 2 && elem_bytes != 4) return fail(XDIT_ERR_UNSUPPORTED, "elem_bytes must be 2 or 4");
   Plan P;
   XRET(make_plan(B, H, S_txt, S_img, D, c->u, c->r, c->rank, &P));
   const Sizes s = sizes_for(P, B, D, elem_bytes);
-  XRET(ensure(&c->uly_send, s.uly3));
+  void* before[kNHandles] = {};
+  for (int k = 0; k < kHFlags; ++k) before[k] = exported(c, k)->p;
+  if (c->transport == XDIT_TRANSPORT_PEER) XCUDA(cudaDeviceSynchronize());  // peers' writes drained
+  XRET(ensure(&c->uly_send, s.uly3 * (c->transport == XDIT_TRANSPORT_NCCL)));
   XRET(ensure(&c->uly_recv, s.uly3));
   XRET(ensure(&c->qblk, s.qblk));
   for (int a = 0; a < 2; ++a)
@@ -580,6 +840,8 @@ int xdit_comm_reserve(xdit_comm_t c, int B, int H, int S_txt, int S_img, int D, 
   XRET(ensure(&c->osend, s.ochunk * P.u * (P.u > 1)));
   XRET(ensure(&c->orecv, s.ochunk * P.u * (P.u > 1)));
   if (elem_bytes == 2) XRET(ensure(&c->tail, xdit::attn_scratch_floats(D) * sizeof(float)));
+  for (int k = 0; k < kHFlags; ++k)
+    if (exported(c, k)->p != before[k]) c->connected = false;  // peers must map the new buffers
   return XDIT_OK;
 }
 
@@ -595,6 +857,9 @@ int xdit_comm_info(xdit_comm_t c, int* nranks, int* rank, int* ulysses, int* rin
 int xdit_comm_destroy(xdit_comm_t c) {
   if (!c) return XDIT_OK;
   if (c->side) cudaStreamSynchronize(c->side);
+  if (c->transport == XDIT_TRANSPORT_PEER) cudaDeviceSynchronize();
+  close_peers(c);
+  if (c->flags) cudaFree(c->flags);
   Buf* bufs[] = {&c->uly_send, &c->uly_recv, &c->qblk, &c->kv[0][0], &c->kv[0][1], &c->kv[1][0],
                  &c->kv[1][1], &c->oacc, &c->lacc, &c->otmp, &c->ltmp, &c->osend, &c->orecv, &c->tail};
   for (Buf* b : bufs)

@@ -14,8 +14,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("XDIT_LIB") or os.path.join(HERE, "libxdit_usp.so")  # XDIT_LIB: A/B builds
 
 XDIT_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "DIVISIBILITY", 4: "COMM_MISMATCH",
-               5: "EMPTY_SHARD", 6: "ALIGNMENT", 7: "CUDA", 8: "NCCL", 9: "WORKSPACE"}
+               5: "EMPTY_SHARD", 6: "ALIGNMENT", 7: "CUDA", 8: "NCCL", 9: "WORKSPACE", 10: "NOT_CONNECTED"}
 NCCL_UNIQUE_ID_BYTES = 128
+PEER_BLOB_BYTES = 1024  # XDIT_PEER_BLOB_BYTES
+TRANSPORTS = {"nccl": 0, "peer": 1}  # XDIT_TRANSPORT_NCCL / XDIT_TRANSPORT_PEER
 
 
 class XditError(RuntimeError):
@@ -66,6 +68,10 @@ _SIGS = {
     "xdit_nccl_unique_id": ([_vp], _i),
     "xdit_comm_init": ([_vp, _i, _i, _i, _i, ctypes.POINTER(_vp)], _i),
     "xdit_comm_create": ([_vp, _i, _i, ctypes.POINTER(_vp)], _i),
+    "xdit_comm_init_peer": ([_i, _i, _i, _i, ctypes.POINTER(_vp)], _i),
+    "xdit_comm_peer_export": ([_vp, _vp], _i),
+    "xdit_comm_peer_connect": ([_vp, _vp], _i),
+    "xdit_comm_transport": ([_vp], _i),
     "xdit_comm_reserve": ([_vp, _i, _i, _i, _i, _i, _i], _i),
     "xdit_comm_info": ([_vp] + [ctypes.POINTER(_i)] * 4, _i),
     "xdit_comm_destroy": ([_vp], _i),
@@ -152,47 +158,78 @@ def _stream(stream=None) -> int:
 
 
 class Comm:
-    """One SP group (= one CFG group): ulysses x ring mesh, NCCL sub-communicators, workspace.
+    """One SP group (= one CFG group): ulysses x ring mesh, transport, workspace.
 
-    With ulysses*ring == 1 no NCCL object is created.  Otherwise rank 0 of `group` (a
-    torch.distributed process group, default WORLD) creates an NCCL unique id, which is broadcast
-    with torch.distributed; every rank then calls xdit_comm_init on its current CUDA device.
+    transport="peer" (default): the library's peer-memory transport -- ranks map each other's
+    receive buffers (CUDA IPC over NVLink/NVSwitch) and order their streams with device flags;
+    torch.distributed (`group`, any backend) only carries the one-time handle exchange.
+    transport="nccl": rank 0 of `group` creates an NCCL unique id, broadcast with torch.distributed,
+    and every rank calls xdit_comm_init (the library's own NCCL communicators).
+    With ulysses*ring == 1 neither is needed and no communication object is made.
     """
 
-    def __init__(self, ulysses: int = 1, ring: int = 1, group=None):
-        self.ulysses, self.ring = ulysses, ring
+    def __init__(self, ulysses: int = 1, ring: int = 1, group=None, transport: str = "peer"):
+        if transport not in TRANSPORTS:
+            raise XditError(1, "Comm", f"transport must be one of {sorted(TRANSPORTS)}, got {transport!r}")
+        self.ulysses, self.ring, self.group = ulysses, ring, group
         n = ulysses * ring
         h = _vp()
+        self.transport = transport if n > 1 else "nccl"
         if n == 1:
             _check(lib().xdit_comm_init(None, 1, 0, 1, 1, ctypes.byref(h)), "xdit_comm_init")
             self.rank = 0
         else:
-            import torch
             import torch.distributed as dist
             rank = dist.get_rank(group)
             if dist.get_world_size(group) != n:
                 raise XditError(4, "Comm", f"group size {dist.get_world_size(group)} != ulysses*ring={n}")
-            buf = (ctypes.c_uint8 * NCCL_UNIQUE_ID_BYTES)()
-            if rank == 0:
-                _check(lib().xdit_nccl_unique_id(ctypes.cast(buf, _vp)), "xdit_nccl_unique_id")
-            obj = [bytes(buf)]
-            src = dist.get_global_rank(group, 0) if group is not None else 0
-            dist.broadcast_object_list(obj, src=src, group=group)
-            ctypes.memmove(buf, obj[0], NCCL_UNIQUE_ID_BYTES)
-            _check(lib().xdit_comm_init(ctypes.cast(buf, _vp), n, rank, ulysses, ring, ctypes.byref(h)),
-                   "xdit_comm_init")
+            if transport == "peer":
+                _check(lib().xdit_comm_init_peer(n, rank, ulysses, ring, ctypes.byref(h)), "xdit_comm_init_peer")
+            else:
+                buf = (ctypes.c_uint8 * NCCL_UNIQUE_ID_BYTES)()
+                if rank == 0:
+                    _check(lib().xdit_nccl_unique_id(ctypes.cast(buf, _vp)), "xdit_nccl_unique_id")
+                obj = [bytes(buf)]
+                src = dist.get_global_rank(group, 0) if group is not None else 0
+                dist.broadcast_object_list(obj, src=src, group=group)
+                ctypes.memmove(buf, obj[0], NCCL_UNIQUE_ID_BYTES)
+                _check(lib().xdit_comm_init(ctypes.cast(buf, _vp), n, rank, ulysses, ring, ctypes.byref(h)),
+                       "xdit_comm_init")
             self.rank = rank
         self.handle = h
         self._reserved = None
 
     def reserve(self, B: int, H: int, S_txt: int, S_img: int, D: int, elem_bytes: int = 2):
+        """Collective when the shape changes (every rank, same scalars): reserve the workspace and,
+        for the peer transport, exchange and map the peers' buffers."""
         key = (B, H, S_txt, S_img, D, elem_bytes)
         if self._reserved != key:
+            peer = self.transport == "peer"
+            if peer:  # nobody may still be writing into a buffer the reserve could reallocate
+                import torch
+                import torch.distributed as dist
+                torch.cuda.synchronize()
+                dist.barrier(group=self.group)
             _check(lib().xdit_comm_reserve(self.handle, *key), "xdit_comm_reserve")
+            if peer:
+                self.connect()
             self._reserved = key
         return self
 
+    def connect(self):
+        """Peer transport: export this rank's buffer descriptor, all-gather them, map the peers'."""
+        import torch.distributed as dist
+        blob = (ctypes.c_uint8 * PEER_BLOB_BYTES)()
+        _check(lib().xdit_comm_peer_export(self.handle, ctypes.cast(blob, _vp)), "xdit_comm_peer_export")
+        n = self.ulysses * self.ring
+        blobs = [None] * n
+        dist.all_gather_object(blobs, bytes(blob), group=self.group)
+        allb = (ctypes.c_uint8 * (PEER_BLOB_BYTES * n)).from_buffer_copy(b"".join(blobs))
+        _check(lib().xdit_comm_peer_connect(self.handle, ctypes.cast(allb, _vp)), "xdit_comm_peer_connect")
+
     def destroy(self):
+        """Frees the handle.  Peer transport: every rank must have drained its streams first (the
+        peers may still be writing into this rank's buffers) -- call collectively, after a barrier."""
         if self.handle:
             lib().xdit_comm_destroy(self.handle)
             self.handle = None

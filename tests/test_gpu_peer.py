@@ -1,0 +1,71 @@
+"""Multi-process USP through the peer-memory transport.
+
+The real multi-rank call path -- one process per SP rank, the library's peer transport moving the
+Ulysses all-to-all (pack kernel storing into the peers' receive buffers), the ring K/V
+rotation (peer copies into the successor's free slot while attention runs) and the O/LSE
+return, with cross-rank stream ordering through device flags -- run with all ranks on the one GPU
+of the test box (CUDA IPC works between processes on one device exactly as between NVLink peers).
+Every rank checks its own rows against the fp64 oracle for every (ulysses, ring) factorisation of
+the world size, bitwise determinism of a repeated call, and the retained KV
+buffer (NEXT 1, reading R2).  Shapes change between cases, so re-reservation + re-connection is
+exercised too.
+"""
+import json
+import multiprocessing as mp
+import os
+import socket
+import tempfile
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+# (B, H, S_txt, S_img, D, dtype, check kv_keep): ragged text + image shards, every bf16 head dim,
+# the fp32 mode; H = 8 divides every Ulysses degree up to 8.
+CASES = [(2, 8, 33, 400, 64, "bf16", True), (1, 8, 0, 700, 72, "bf16", False),
+         (1, 8, 17, 300, 128, "bf16", True), (1, 8, 9, 150, 64, "f32", False)]
+SPLITS = {2: [(2, 1), (1, 2)], 4: [(2, 2), (4, 1), (1, 4)], 8: [(2, 4), (4, 2), (8, 1), (1, 8)]}
+
+
+def _port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _run_world(world: int, splits, cases, timeout: float = 900):
+    from tests import _peer_worker
+    ctx = mp.get_context("spawn")
+    port = _port()
+    with tempfile.TemporaryDirectory() as d:
+        procs = [ctx.Process(target=_peer_worker.run, args=(g, world, port, splits, cases, d)) for g in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout)
+        hung = [g for g, p in enumerate(procs) if p.is_alive()]
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+        assert not hung, f"ranks {hung} did not finish within {timeout}s"
+        out = []
+        for g in range(world):
+            path = os.path.join(d, f"rank{g}.json")
+            assert os.path.exists(path), f"rank {g} wrote no result (exit code {procs[g].exitcode})"
+            with open(path) as f:
+                out.append(json.load(f))
+    for r in out:
+        assert r["error"] is None, f"rank {r['rank']}:\n{r['error']}"
+        assert len(r["checks"]) == len(splits) * len(cases)
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_peer_transport_usp_all_splits(world):
+    _run_world(world, SPLITS[world], CASES)
+
+
+def test_peer_transport_toy_2x2_config0():
+    """BASELINE.json configs[0]: toy DiT attention, B=1, H=4, D=64, 1024 tokens, Ulysses=2 x Ring=2,
+    four real processes, against the unsplit fp64 oracle."""
+    _run_world(4, [(2, 2)], [(1, 4, 0, 1024, 64, "bf16", True)])
