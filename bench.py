@@ -8,8 +8,11 @@ A "step" is one USP attention call (pack -> all-to-all -> 
 attention + LSE merge -> reverse all-to-all) over one batch of synthetic Q/K/V of the workload.
 N=1 default workload: Flux.1 4096px (B=1, H=24, D=128, 512 text + 65536 image tokens), the shape
 BASELINE.json's north_star targets.  Multi-GPU: one process per GPU under
-torchrun, NCCL; the same global problem is split over N ranks (strong scaling), CFG groups when the
-workload has them.  Rank 0 prints ONE JSON line.
+torchrun (torch.distributed/NCCL for the barrier and the max over ranks); the library moves the USP
+bytes itself (peer-memory transport, or NCCL with --transport nccl); the same global problem is
+split over N ranks (strong scaling), CFG groups when the workload has them.  Rank 0 prints ONE JSON
+line.  XDIT_SHARE_GPU=1 puts every rank on cuda:0 with a gloo process group -- a functional check of
+the N > 1 path on a 1-GPU box (its timings are not scaling numbers).
 """
 from __future__ import annotations
 
@@ -40,6 +43,8 @@ def parse():
     ap.add_argument("--ulysses", type=int, default=0)
     ap.add_argument("--ring", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="multi-rank byte movement: the library's peer-memory transport or NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     return ap.parse_args()
@@ -203,10 +208,16 @@ def main():
     from paper_2411_01738_b200.inputs import qkv, seed_for
 
     N = world
+    share = os.environ.get("XDIT_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if N > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     cfg, u, r = default_split(N, w.H, w.cfg)
     if args.ulysses or args.ring:
         u = args.ulysses or max(1, N // cfg // max(1, args.ring))
@@ -220,7 +231,7 @@ def main():
         group = groups[cfg_group]
     # batch handled by this CFG group: CFG splits the 2-latent batch
     B = w.B * w.cfg // cfg
-    comm = usp.Comm(u, r, group=group if sp > 1 else None)
+    comm = usp.Comm(u, r, group=group if sp > 1 else None, transport=args.transport)
     comm.reserve(B, w.H, w.S_txt, w.S_img, w.D, 2)
     to, tl, io, il = usp.shard(w.S_txt, w.S_img, sp, sp_rank)
     L = tl + il
@@ -244,7 +255,7 @@ def main():
     def max_over_ranks(x: float) -> float:
         if N == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -407,6 +418,8 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": w.name, "B": w.B * w.cfg, "H": w.H, "D": w.D, "S_txt": w.S_txt,
                        "S_img": w.S_img, "cfg": cfg, "ulysses": u, "ring": r,
+                       "transport": comm.transport if sp > 1 else None,
+                       **({"shared_gpu": True} if share and N > 1 else {}),
                        "l2": "flushed between steps" if flush else "inputs larger than L2"},
             "ms_per_layer": ms,
             "tflops_per_gpu": tflops / N,
@@ -429,6 +442,9 @@ def main():
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
+    torch.cuda.synchronize()
+    if N > 1:  # peers may still map this rank's buffers: everyone drained before anyone frees
+        dist.barrier()
     comm.destroy()
     if N > 1:
         dist.barrier()
