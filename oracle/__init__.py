@@ -12,6 +12,8 @@ Functions (numpy float64 arrays, layouts as in xdit_oracle.c):
   usp_emulate(q, k, v, S_txt, u, r) -> out, lse                      (readings C5-C9)
   kv_keep(k, v, S_txt, u, r, g) -> [2,B,H/u,S,D]  KV buffer rank g retains (NEXT 1)
   cfg_combine(eps_cond, eps_uncond, g) -> eps_uncond + g (eps_cond - eps_uncond)  (NEXT 2)
+  pipefusion.*  (submodule, numpy fp64): PipeFusion on a synthetic DiT stack -- patch bounds, the
+                staleness replay and the stale-KV numerics (NEXT 3, reading R4)
 """
 from __future__ import annotations
 
