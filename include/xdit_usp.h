@@ -325,6 +325,36 @@ XDIT_API int xdit_kv_retain(const void* k_blk, const void* v_blk, void* kv_keep,
                             int S_total, int seq_off, int D, int64_t src_b, int64_t src_s, int64_t src_h,
                             int elem_bytes, xdit_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------ */
+/* PipeFusion (§4.1.2; reading R4).  The stage-  */
+/* local work of one PipeFusion micro-step on a synthetic DiT stack: one block applied to one     */
+/* patch, attending over the block's KV buffer in which the patch's own K,V are fresh and the     */
+/* other patches' are whatever the buffer holds -- this step's for patches already processed at   */
+/* this block, the previous step's for the rest ("uses stale activations from the previous        */
+/* timestep to provide context").  The pipeline schedule (which patch on which stage   */
+/* when, P2P of patch activations) is the caller's (paper_2411_01738_b200/pipefusion.py).          */
+/* ------------------------------------------------------------------------------------------ */
+
+/* Device workspace xdit_pf_block needs for a patch of n rows (0 for invalid arguments). */
+XDIT_API size_t xdit_pf_block_workspace_bytes(int B, int n, int H, int D, int dtype);
+
+/* Synthetic DiT block on one patch (reading R4):
+ *   K,V buffer rows [off, off+n) <- h*wk, h*wv;   h <- h + g * softmax((h*wq) Kbuf^T / sqrt(D)) Vbuf
+ * h      : DEVICE [B][n][H][D], the patch's hidden rows (updated in place)
+ * kv_buf : DEVICE [2][B][H][S][D] (K then V, head-major) -- the block's buffer over the whole sequence
+ * w      : DEVICE fp32 [4][H][D] = (wq, wk, wv, g)
+ * work   : DEVICE scratch of >= xdit_pf_block_workspace_bytes(B, n, H, D, dtype) bytes
+ * dtype  : 0 = bf16 h / kv_buf (tcgen05 attention, D in {64,72,128}), 1 = fp32 (SIMT, D % 8 == 0, <= 256)
+ * Products are formed in fp32 and rounded once; the attention output stays fp32 until the residual.
+ * Stream-ordered on `stream`, no allocation, no host sync.
+ * Errors: INVALID_ARG, UNSUPPORTED, ALIGNMENT (16-byte pointers), WORKSPACE, CUDA. */
+XDIT_API int xdit_pf_block(void* h, void* kv_buf, const float* w, void* work, size_t work_bytes, int B, int H, int S,
+                           int off, int n, int D, int dtype, xdit_stream_t stream);
+
+/* Synthetic sampler step (reading R4): x <- x - sigma * eps over n elements (n % 8 == 0), DEVICE
+ * buffers of dtype 0 (bf16) or 1 (fp32); fp32 math, one rounding.  Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype, xdit_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -63,6 +63,12 @@ cudaError_t launch_kv_retain(const void* k, const void* v, void* kv_keep, int B,
 cudaError_t launch_cfg_combine(const void* c, const void* u, void* o, int64_t n, float g, int dtype,
                                cudaStream_t st);
 
+// SURVEY §8(f) NEXT 3, PipeFusion on a synthetic DiT stack (pipefusion.cu).
+size_t pf_workspace_bytes(int B, int n, int H, int D, int dtype);
+cudaError_t launch_pf_block(void* h, void* kv, const float* w, void* work, int B, int H, int S, int off, int n,
+                            int D, int dtype, cudaStream_t st);
+cudaError_t launch_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype, cudaStream_t st);
+
 // Device-side row-map resolution shared by every epilogue that writes through an xdit_rowmap.
 struct RowDst {
   int64_t o_off;  // element offset of (b, row, h, 0)

@@ -950,6 +950,37 @@ int xdit_cfg_tail(const void* eps_local, void* eps_gather, void* eps_out, int64_
   return XDIT_OK;
 }
 
+size_t xdit_pf_block_workspace_bytes(int B, int n, int H, int D, int dtype) {
+  if (B < 0 || n < 0 || H < 1 || D < 1 || (dtype != 0 && dtype != 1)) return 0;
+  return xdit::pf_workspace_bytes(B, n, H, D, dtype);
+}
+
+int xdit_pf_block(void* h, void* kv_buf, const float* w, void* work, size_t work_bytes, int B, int H, int S, int off,
+                  int n, int D, int dtype, xdit_stream_t stream) {
+  if (!h || !kv_buf || !w || !work) return fail(XDIT_ERR_INVALID_ARG, "xdit_pf_block: NULL pointer");
+  if (B < 0 || H < 1 || S < 1 || n < 0 || off < 0 || off + n > S || D < 1 || (dtype != 0 && dtype != 1))
+    return fail(XDIT_ERR_INVALID_ARG, "xdit_pf_block: bad sizes (B=%d H=%d S=%d off=%d n=%d D=%d dtype=%d)", B, H, S,
+                off, n, D, dtype);
+  if (dtype == 0 && D != 64 && D != 72 && D != 128)
+    return fail(XDIT_ERR_UNSUPPORTED, "bf16 path supports D in {64,72,128}, got %d", D);
+  if (dtype == 1 && (D > 256 || D % 8))
+    return fail(XDIT_ERR_UNSUPPORTED, "fp32 path supports D %% 8 == 0 and D <= 256, got %d", D);
+  if (!aligned16(h) || !aligned16(kv_buf) || !aligned16(w) || !aligned16(work))
+    return fail(XDIT_ERR_ALIGNMENT, "xdit_pf_block: pointers must be 16-byte aligned");
+  if (work_bytes < xdit::pf_workspace_bytes(B, n, H, D, dtype))
+    return fail(XDIT_ERR_WORKSPACE, "xdit_pf_block: workspace of %zu bytes < %zu", work_bytes,
+                xdit::pf_workspace_bytes(B, n, H, D, dtype));
+  XCUDA(xdit::launch_pf_block(h, kv_buf, w, work, B, H, S, off, n, D, dtype, reinterpret_cast<cudaStream_t>(stream)));
+  return XDIT_OK;
+}
+
+int xdit_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype, xdit_stream_t stream) {
+  if (!x || !eps || n < 0 || (dtype != 0 && dtype != 1)) return fail(XDIT_ERR_INVALID_ARG, "xdit_pf_sampler: bad arguments");
+  if (!aligned16(x) || !aligned16(eps) || n % 8) return fail(XDIT_ERR_ALIGNMENT, "xdit_pf_sampler: 16-byte alignment, n %% 8 == 0");
+  XCUDA(xdit::launch_pf_sampler(x, eps, n, sigma, dtype, reinterpret_cast<cudaStream_t>(stream)));
+  return XDIT_OK;
+}
+
 int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,
                   int Sq, int Skv, int D, int64_t q_b, int64_t q_s, int64_t q_h, int64_t kv_b,
                   int64_t kv_s, int64_t kv_h, const xdit_rowmap* omap, int dtype, int out_f32,

@@ -88,6 +88,9 @@ _SIGS = {
     "xdit_uly_pack": ([_vp, _vp] + [_i] * 9 + [_vp], _i),
     "xdit_uly_unpack": ([_vp, _vp] + [_i] * 5 + [ctypes.POINTER(_i), _i, _i, _i, _vp], _i),
     "xdit_uly_unpack_out": ([_vp, _vp, _i64, _i64, _vp, _vp] + [_i] * 7 + [_vp], _i),
+    "xdit_pf_block_workspace_bytes": ([_i] * 5, ctypes.c_size_t),
+    "xdit_pf_block": ([_vp] * 4 + [ctypes.c_size_t] + [_i] * 7 + [_vp], _i),
+    "xdit_pf_sampler": ([_vp, _vp, _i64, ctypes.c_float, _i, _vp], _i),
 }
 
 
