@@ -150,6 +150,30 @@ XDIT_API int xdit_comm_peer_connect(xdit_comm_t comm, const void* blobs);
 /* XDIT_TRANSPORT_NCCL or XDIT_TRANSPORT_PEER; -1 for NULL. */
 XDIT_API int xdit_comm_transport(xdit_comm_t comm);
 
+/* ---- Peer transport mailbox: point-to-point messages between any two ranks of the handle, for
+ * the patch activations PipeFusion passes between stages "via asynchronous P2P" (NEXT 3) and
+ * the CFG tail's gather (NEXT 2).  Every rank owns nranks regions of bytes_per_src bytes
+ * (region s receives from rank s).  Like xdit_comm_reserve, growing the mailbox clears the
+ * connection: export / exchange / connect again (all ranks, after a drained barrier).
+ * Ordering is the caller's protocol of monotonically increasing 32-bit tags per (sender, receiver):
+ *   sender:   [xdit_p2p_wait_ack(receiver, t-k)] -> xdit_p2p_put(receiver, ..., t)
+ *   receiver: xdit_p2p_wait(sender, t) -> consume its region -> xdit_p2p_ack(sender, t)
+ * All four are stream-ordered (peer copy + cuStreamWriteValue32 / cuStreamWaitValue32); tags compare
+ * wraparound-safe (>=).  Errors: INVALID_ARG, NOT_CONNECTED, WORKSPACE (no or too small mailbox), CUDA. */
+XDIT_API int xdit_comm_mailbox_reserve(xdit_comm_t comm, size_t bytes_per_src);
+/* DEVICE address and size of this rank's region that receives from rank `src`. */
+XDIT_API int xdit_p2p_mailbox(xdit_comm_t comm, int src, void** ptr, size_t* bytes);
+/* Copy `bytes` from DEVICE `src` into rank dst's region for this rank at dst_off, then set this rank's
+ * data flag on dst to `tag` -- ordered after all prior work of `stream`. */
+XDIT_API int xdit_p2p_put(xdit_comm_t comm, int dst, const void* src, size_t bytes, size_t dst_off, uint32_t tag,
+                          xdit_stream_t stream);
+/* Later work of `stream` waits until sender `src`'s data flag here is >= tag. */
+XDIT_API int xdit_p2p_wait(xdit_comm_t comm, int src, uint32_t tag, xdit_stream_t stream);
+/* Tell `sender` (after all prior work of `stream`) that its messages up to `tag` are consumed. */
+XDIT_API int xdit_p2p_ack(xdit_comm_t comm, int sender, uint32_t tag, xdit_stream_t stream);
+/* Later work of `stream` waits until `receiver` acknowledged tag (>=). */
+XDIT_API int xdit_p2p_wait_ack(xdit_comm_t comm, int receiver, uint32_t tag, xdit_stream_t stream);
+
 /* Allocates (or grows) the device workspace for a problem: Ulysses send/recv buffers, the
  * unpacked Q block, two ring KV slots, fp32 ring accumulators.  Call once per shape before the
  * hot loop (all ranks, same scalars); xdit_usp_attention never allocates, so the call path is

@@ -204,8 +204,11 @@ int check_map_align(const xdit_rowmap* m, int vec_elems) {
 
 namespace {
 // Peer-memory transport: exported buffers (blob handle index) and flag words.
-enum { kHUly = 0, kHORecv = 1, kHKV = 2 /* kHKV + 2*slot + (0 K, 1 V) */, kHFlags = 6, kNHandles = 7 };
-enum { kFA2A = 0, kFO = 8, kFData = 16, kFCredit = 18, kFlagWords = 32 };
+enum { kHUly = 0, kHORecv = 1, kHKV = 2 /* kHKV + 2*slot + (0 K, 1 V) */, kHFlags = 6, kHMbox = 7, kNHandles = 8 };
+// flag words: Ulysses data, O return, ring data / credit, mailbox data / ack (per source rank),
+// CFG tail data / ack
+enum { kFA2A = 0, kFO = 8, kFData = 16, kFCredit = 18, kFP2P = 32, kFAck = 40, kFCfg = 48, kFCfgAck = 50,
+       kFlagWords = 64 };
 constexpr uint32_t kBlobMagic = 0x31504458u;  // "XDP1"
 struct PeerBlob {
   uint32_t magic;
@@ -249,12 +252,14 @@ struct xdit_comm_s {
   uint32_t epoch = 0;         // peer transport: calls issued (identical on every rank)
   bool connected = false;
   std::vector<PeerMap> peer;  // peer transport: per SP rank (self = local pointers)
+  size_t mbox_region = 0;     // peer transport: mailbox bytes per source rank
+  uint32_t cfg_epoch = 0;     // peer transport: xdit_cfg_tail calls issued
   ncclComm_t sp = nullptr, uly = nullptr, ring = nullptr;
   bool own_sp = false;
   cudaStream_t side = nullptr;
   cudaEvent_t ev_start = nullptr, ev_a2a = nullptr, ev_o = nullptr, ev_o_a2a = nullptr;
   cudaEvent_t ev_kdone[2] = {nullptr, nullptr}, ev_recv[2] = {nullptr, nullptr};
-  Buf uly_send, uly_recv, qblk, kv[2][2], oacc, lacc, otmp, ltmp, osend, orecv, tail;
+  Buf uly_send, uly_recv, qblk, kv[2][2], oacc, lacc, otmp, ltmp, osend, orecv, tail, mbox;
 };
 
 namespace {
@@ -311,6 +316,7 @@ Buf* exported(xdit_comm_s* c, int k) {
     case kHKV + 1: return &c->kv[0][1];
     case kHKV + 2: return &c->kv[1][0];
     case kHKV + 3: return &c->kv[1][1];
+    case kHMbox: return &c->mbox;
     default: return nullptr;
   }
 }
@@ -793,12 +799,12 @@ int xdit_comm_peer_connect(xdit_comm_t c, const void* blobs) {
   close_peers(c);
   c->peer.assign(c->nranks, PeerMap{});
   const int i = c->rank / c->u, j = c->rank % c->u;
-  const int nxt = ((i + 1) % c->r) * c->u + j, prv = ((i - 1 + c->r) % c->r) * c->u + j;
+  const int nxt = ((i + 1) % c->r) * c->u + j;
   for (int q = 0; q < c->nranks; ++q) {
     PeerMap& m = c->peer[q];
-    const bool uly_peer = q / c->u == i && c->u > 1, ring_nb = c->r > 1 && (q == nxt || q == prv);
+    const bool uly_peer = q / c->u == i && c->u > 1;
     for (int k = 0; k < kNHandles; ++k) {
-      const bool want = k == kHFlags ? (uly_peer || ring_nb)
+      const bool want = (k == kHFlags || k == kHMbox) ? true  // any rank may message any rank
                                      : (k < kHKV ? uly_peer : (c->r > 1 && q == nxt));
       if (!want || !(bl[q].valid & (1u << k))) continue;
       m.bytes[k] = bl[q].bytes[k];
@@ -819,6 +825,70 @@ int xdit_comm_peer_connect(xdit_comm_t c, const void* blobs) {
   return XDIT_OK;
 }
 
+int xdit_comm_mailbox_reserve(xdit_comm_t c, size_t bytes_per_src) {
+  if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
+  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
+  const size_t region = (bytes_per_src + 255) & ~size_t(255);
+  if (region <= c->mbox_region) return XDIT_OK;
+  XCUDA(cudaDeviceSynchronize());  // peers' writes into the old mailbox drained (caller: after a barrier)
+  XRET(ensure(&c->mbox, region * c->nranks));
+  c->mbox_region = region;
+  c->connected = false;  // peers must map the new mailbox
+  return XDIT_OK;
+}
+
+int xdit_p2p_mailbox(xdit_comm_t c, int src, void** ptr, size_t* bytes) {
+  if (!c || !ptr || src < 0 || src >= c->nranks) return fail(XDIT_ERR_INVALID_ARG, "xdit_p2p_mailbox: bad arguments");
+  if (!c->mbox.p) return fail(XDIT_ERR_WORKSPACE, "no mailbox reserved (xdit_comm_mailbox_reserve)");
+  *ptr = static_cast<char*>(c->mbox.p) + size_t(src) * c->mbox_region;
+  if (bytes) *bytes = c->mbox_region;
+  return XDIT_OK;
+}
+
+namespace {
+int p2p_check(xdit_comm_s* c, int peer_rank) {
+  if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
+  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
+  if (!c->connected) return fail(XDIT_ERR_NOT_CONNECTED, "peer transport: connect after (re)reserving");
+  if (peer_rank < 0 || peer_rank >= c->nranks) return fail(XDIT_ERR_INVALID_ARG, "rank %d out of range", peer_rank);
+  return XDIT_OK;
+}
+}  // namespace
+
+int xdit_p2p_put(xdit_comm_t c, int dst, const void* src, size_t bytes, size_t dst_off, uint32_t tag,
+                 xdit_stream_t stream) {
+  XRET(p2p_check(c, dst));
+  if (!src && bytes) return fail(XDIT_ERR_INVALID_ARG, "xdit_p2p_put: src is NULL");
+  if (dst_off + bytes > c->mbox_region)
+    return fail(XDIT_ERR_WORKSPACE, "xdit_p2p_put: %zu bytes at offset %zu exceed the %zu-byte mailbox region", bytes,
+                dst_off, c->mbox_region);
+  const PeerMap& m = c->peer[dst];
+  if (!m.ptr[kHMbox] || !m.ptr[kHFlags]) return fail(XDIT_ERR_WORKSPACE, "rank %d has no mapped mailbox", dst);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (bytes)
+    XCUDA(cudaMemcpyAsync(static_cast<char*>(m.ptr[kHMbox]) + size_t(c->rank) * c->mbox_region + dst_off, src, bytes,
+                          cudaMemcpyDefault, st));
+  return post_flag(st, static_cast<uint32_t*>(m.ptr[kHFlags]) + kFP2P + c->rank, tag);
+}
+
+int xdit_p2p_wait(xdit_comm_t c, int src, uint32_t tag, xdit_stream_t stream) {
+  XRET(p2p_check(c, src));
+  return wait_flag(reinterpret_cast<cudaStream_t>(stream), c->flags + kFP2P + src, tag);
+}
+
+int xdit_p2p_ack(xdit_comm_t c, int sender, uint32_t tag, xdit_stream_t stream) {
+  XRET(p2p_check(c, sender));
+  const PeerMap& m = c->peer[sender];
+  if (!m.ptr[kHFlags]) return fail(XDIT_ERR_WORKSPACE, "rank %d's flags are not mapped", sender);
+  return post_flag(reinterpret_cast<cudaStream_t>(stream), static_cast<uint32_t*>(m.ptr[kHFlags]) + kFAck + c->rank,
+                   tag);
+}
+
+int xdit_p2p_wait_ack(xdit_comm_t c, int receiver, uint32_t tag, xdit_stream_t stream) {
+  XRET(p2p_check(c, receiver));
+  return wait_flag(reinterpret_cast<cudaStream_t>(stream), c->flags + kFAck + receiver, tag);
+}
+
 int xdit_comm_reserve(xdit_comm_t c, int B, int H, int S_txt, int S_img, int D, int elem_bytes) {
   if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
   if (elem_bytes != 2 && elem_bytes != 4) return fail(XDIT_ERR_UNSUPPORTED, "elem_bytes must be 2 or 4");
@@ -826,7 +896,7 @@ int xdit_comm_reserve(xdit_comm_t c, int B, int H, int S_txt, int S_img, int D, 
   XRET(make_plan(B, H, S_txt, S_img, D, c->u, c->r, c->rank, &P));
   const Sizes s = sizes_for(P, B, D, elem_bytes);
   void* before[kNHandles] = {};
-  for (int k = 0; k < kHFlags; ++k) before[k] = exported(c, k)->p;
+  for (int k = 0; k < kHFlags; ++k) before[k] = exported(c, k)->p;  // (the mailbox is not reallocated here)
   if (c->transport == XDIT_TRANSPORT_PEER) XCUDA(cudaDeviceSynchronize());  // peers' writes drained
   XRET(ensure(&c->uly_send, s.uly3 * (c->transport == XDIT_TRANSPORT_NCCL)));
   XRET(ensure(&c->uly_recv, s.uly3));
@@ -861,7 +931,8 @@ int xdit_comm_destroy(xdit_comm_t c) {
   close_peers(c);
   if (c->flags) cudaFree(c->flags);
   Buf* bufs[] = {&c->uly_send, &c->uly_recv, &c->qblk, &c->kv[0][0], &c->kv[0][1], &c->kv[1][0],
-                 &c->kv[1][1], &c->oacc, &c->lacc, &c->otmp, &c->ltmp, &c->osend, &c->orecv, &c->tail};
+                 &c->kv[1][1], &c->oacc, &c->lacc, &c->otmp, &c->ltmp, &c->osend, &c->orecv, &c->tail,
+                 &c->mbox};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->uly) ncclCommDestroy(c->uly);
@@ -944,6 +1015,31 @@ int xdit_cfg_tail(const void* eps_local, void* eps_gather, void* eps_out, int64_
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // All-gather of the two branches' predictions over the cfg pair (rank 0 = conditional, rank 1 =
   // unconditional: reading R3), then the combine on every rank.
+  const size_t bytes = size_t(n) * eb;
+  if (comm->transport == XDIT_TRANSPORT_PEER) {
+    // peer transport: eps_local -> the peer's mailbox (after the peer acknowledged the previous
+    // call's), flag; own copy into eps_gather[rank]; wait for the peer's flag, copy its prediction out
+    // of the mailbox into eps_gather[1 - rank], acknowledge.
+    if (!comm->connected) return fail(XDIT_ERR_NOT_CONNECTED, "peer transport: connect after (re)reserving");
+    if (bytes > comm->mbox_region)
+      return fail(XDIT_ERR_WORKSPACE, "cfg_tail: %zu bytes exceed the %zu-byte mailbox region "
+                  "(xdit_comm_mailbox_reserve)", bytes, comm->mbox_region);
+    const int me = comm->rank, other = 1 - me;
+    const uint32_t e = ++comm->cfg_epoch;
+    const PeerMap& m = comm->peer[other];
+    char* gb = static_cast<char*>(eps_gather);
+    XRET(wait_flag(st, comm->flags + kFCfgAck + other, e - 1));
+    XCUDA(cudaMemcpyAsync(static_cast<char*>(m.ptr[kHMbox]) + size_t(me) * comm->mbox_region, eps_local, bytes,
+                          cudaMemcpyDefault, st));
+    XRET(post_flag(st, static_cast<uint32_t*>(m.ptr[kHFlags]) + kFCfg + me, e));
+    XCUDA(cudaMemcpyAsync(gb + size_t(me) * bytes, eps_local, bytes, cudaMemcpyDeviceToDevice, st));
+    XRET(wait_flag(st, comm->flags + kFCfg + other, e));
+    XCUDA(cudaMemcpyAsync(gb + size_t(other) * bytes, static_cast<char*>(comm->mbox.p) + size_t(other) * comm->mbox_region,
+                          bytes, cudaMemcpyDeviceToDevice, st));
+    XRET(post_flag(st, static_cast<uint32_t*>(m.ptr[kHFlags]) + kFCfgAck + me, e));
+    XCUDA(xdit::launch_cfg_combine(gb, gb + bytes, eps_out, n, g, dtype, st));
+    return XDIT_OK;
+  }
   XNCCL(ncclAllGather(eps_local, eps_gather, size_t(n) * eb, ncclUint8, comm->sp, st));
   const char* gb = static_cast<const char*>(eps_gather);
   XCUDA(xdit::launch_cfg_combine(gb, gb + size_t(n) * eb, eps_out, n, g, dtype, st));

@@ -72,6 +72,12 @@ _SIGS = {
     "xdit_comm_peer_export": ([_vp, _vp], _i),
     "xdit_comm_peer_connect": ([_vp, _vp], _i),
     "xdit_comm_transport": ([_vp], _i),
+    "xdit_comm_mailbox_reserve": ([_vp, ctypes.c_size_t], _i),
+    "xdit_p2p_mailbox": ([_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_size_t)], _i),
+    "xdit_p2p_put": ([_vp, _i, _vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint32, _vp], _i),
+    "xdit_p2p_wait": ([_vp, _i, ctypes.c_uint32, _vp], _i),
+    "xdit_p2p_ack": ([_vp, _i, ctypes.c_uint32, _vp], _i),
+    "xdit_p2p_wait_ack": ([_vp, _i, ctypes.c_uint32, _vp], _i),
     "xdit_comm_reserve": ([_vp, _i, _i, _i, _i, _i, _i], _i),
     "xdit_comm_info": ([_vp] + [ctypes.POINTER(_i)] * 4, _i),
     "xdit_comm_destroy": ([_vp], _i),
@@ -229,6 +235,50 @@ class Comm:
         dist.all_gather_object(blobs, bytes(blob), group=self.group)
         allb = (ctypes.c_uint8 * (PEER_BLOB_BYTES * n)).from_buffer_copy(b"".join(blobs))
         _check(lib().xdit_comm_peer_connect(self.handle, ctypes.cast(allb, _vp)), "xdit_comm_peer_connect")
+
+    # ---- peer-transport mailbox (point-to-point messages; see include/xdit_usp.h)
+    def mailbox(self, bytes_per_src: int):
+        """Collective: reserve >= bytes_per_src bytes of mailbox per source rank (re-connects)."""
+        import torch
+        import torch.distributed as dist
+        if self.transport != "peer":
+            raise XditError(1, "Comm.mailbox", "the mailbox needs the peer transport")
+        torch.cuda.synchronize()
+        dist.barrier(group=self.group)
+        _check(lib().xdit_comm_mailbox_reserve(self.handle, int(bytes_per_src)), "xdit_comm_mailbox_reserve")
+        self.connect()
+        return self
+
+    def mailbox_view(self, src: int, shape, dtype, offset: int = 0):
+        """Torch view of this rank's mailbox region from rank `src` (no copy)."""
+        import math
+        import torch
+        p, n = _vp(), ctypes.c_size_t()
+        _check(lib().xdit_p2p_mailbox(self.handle, src, ctypes.byref(p), ctypes.byref(n)), "xdit_p2p_mailbox")
+        esz = torch.empty((), dtype=dtype).element_size()
+        if offset + math.prod(shape) * esz > n.value:
+            raise XditError(9, "mailbox_view", "view exceeds the mailbox region")
+        typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float16: "<f2", torch.uint8: "|u1"}[dtype]
+
+        class _Cai:
+            __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (p.value + offset, False),
+                                        "version": 3, "strides": None}
+        t = torch.as_tensor(_Cai(), device=torch.device("cuda", torch.cuda.current_device()))
+        return t.view(dtype) if dtype == torch.bfloat16 else t
+
+    def put(self, dst: int, src, tag: int, offset: int = 0, stream=None):
+        n = src.numel() * src.element_size()
+        _check(lib().xdit_p2p_put(self.handle, dst, _ptr(src), n, offset, tag & 0xFFFFFFFF, _stream(stream)),
+               "xdit_p2p_put")
+
+    def wait(self, src: int, tag: int, stream=None):
+        _check(lib().xdit_p2p_wait(self.handle, src, tag & 0xFFFFFFFF, _stream(stream)), "xdit_p2p_wait")
+
+    def ack(self, sender: int, tag: int, stream=None):
+        _check(lib().xdit_p2p_ack(self.handle, sender, tag & 0xFFFFFFFF, _stream(stream)), "xdit_p2p_ack")
+
+    def wait_ack(self, receiver: int, tag: int, stream=None):
+        _check(lib().xdit_p2p_wait_ack(self.handle, receiver, tag & 0xFFFFFFFF, _stream(stream)), "xdit_p2p_wait_ack")
 
     def destroy(self):
         """Frees the handle.  Peer transport: every rank must have drained its streams first (the

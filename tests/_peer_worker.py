@@ -66,3 +66,105 @@ def run(rank: int, world: int, port: int, splits, cases, out_dir: str):
         res["error"] = traceback.format_exc()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump(res, f)
+
+
+def run_pipefusion(rank: int, world: int, port: int, cases, out_dir: str):
+    """One PipeFusion stage per process (paper_2411_01738_b200.pipefusion.run_stage) over the peer
+    transport's mailbox; stage 0 checks the final latent against the fp64 staleness oracle and,
+    bitwise, against the in-process N-stage schedule (pipefusion.run)."""
+    res = {"rank": rank, "checks": [], "error": None}
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        from oracle import pipefusion as opf
+        from paper_2411_01738_b200 import pipefusion as pf
+        from paper_2411_01738_b200 import usp
+        from paper_2411_01738_b200.inputs import qkv
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        comm = usp.Comm(world, 1, transport="peer")
+        for ci, (B, S_txt, S_img, H, D, L, T, M, warmup, dt) in enumerate(cases):
+            dtype = torch.float32 if dt == "f32" else torch.bfloat16
+            x0 = qkv(B, S_txt + S_img, H, D, seed=40 + ci, dtype=dtype)[0]
+            rng = np.random.default_rng(40 + ci)
+            W = [tuple(rng.uniform(0.2, 0.4, (H, D)).astype(np.float32) for _ in range(2)) +
+                 (rng.uniform(0.5, 1.5, (H, D)).astype(np.float32), rng.uniform(0.4, 0.8, (H, D)).astype(np.float32))
+                 for _ in range(L)]
+            kw = dict(T=T, M=M, warmup=warmup, sigma=0.5, S_txt=S_txt)
+            x = pf.run_stage(x0.cuda(), W, comm, **kw)
+            torch.cuda.synchronize()
+            if rank == 0:
+                same = pf.run(x0.cuda(), pf.SyntheticDiT(W), stages=world, **kw)
+                torch.cuda.synchronize()
+                assert torch.equal(x, same), "multi-process stages differ from the in-process schedule"
+                W64 = [tuple(w.astype(np.float64) for w in wl) for wl in W]
+                want, _ = opf.pipefusion(x0.double().numpy(), W64, **kw)
+                got = x.double().cpu().numpy()
+                if dt == "f32":
+                    err = float(np.abs(got - want).max() / np.abs(want).max())
+                    assert err <= 1e-3, err
+                else:
+                    err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+                    assert err <= 2e-2, err
+                res["checks"].append({"case": ci, "err": err})
+            dist.barrier()
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        res["error"] = traceback.format_exc()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(res, f)
+
+
+def run_cfg_tail(rank: int, world: int, port: int, cases, out_dir: str):
+    """CFG step tail over the peer transport (NEXT 2): rank 0 = conditional, rank 1 = unconditional
+    branch; every rank's combined eps against oracle.cfg_combine (exact at g = 0, 1)."""
+    res = {"rank": rank, "checks": [], "error": None}
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        import oracle
+        from paper_2411_01738_b200 import usp
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        comm = usp.Comm(2, 1, transport="peer")
+        comm.mailbox(max(n for n, _, _ in cases) * 4)
+        for ci, (n, dt, g) in enumerate(cases):
+            dtype = torch.float32 if dt == "f32" else torch.bfloat16
+            gen = torch.Generator().manual_seed(70 + ci)
+            both = torch.randn(2, n, generator=gen).to(dtype)
+            out = usp.cfg_tail(both[rank].cuda(), g, comm=comm)
+            out2 = usp.cfg_tail(both[rank].cuda(), g, comm=comm)  # second call: the ack protocol
+            torch.cuda.synchronize()
+            c, u = both[0].double().numpy(), both[1].double().numpy()
+            ref = oracle.cfg_combine(c, u, g)
+            got = out.double().cpu().numpy()
+            # same bound as tests/test_gpu_cfg.py: fp32 cancellation (+ one bf16 RNE rounding)
+            bound = (abs(g) * np.abs(c) + abs(1 - g) * np.abs(u)) * 2.0 ** -22 + (np.abs(ref) * 2.0 ** -8 if dt == "bf16" else 0)
+            assert np.all(np.abs(got - ref) <= bound + 1e-30)
+            assert torch.equal(out, out2)
+            if g in (0.0, 1.0):
+                assert torch.equal(out.cpu(), both[1 if g == 0.0 else 0]), "combine not exact at g in {0, 1}"
+            res["checks"].append({"case": ci})
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        res["error"] = traceback.format_exc()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(res, f)

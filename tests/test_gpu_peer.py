@@ -33,12 +33,14 @@ def _port() -> int:
         return s.getsockname()[1]
 
 
-def _run_world(world: int, splits, cases, timeout: float = 900):
+def _run_world(world: int, splits, cases, timeout: float = 900, fn: str = "run"):
     from tests import _peer_worker
     ctx = mp.get_context("spawn")
     port = _port()
+    target = getattr(_peer_worker, fn)
+    args = (lambda g, d: (g, world, port, splits, cases, d)) if fn == "run" else (lambda g, d: (g, world, port, cases, d))
     with tempfile.TemporaryDirectory() as d:
-        procs = [ctx.Process(target=_peer_worker.run, args=(g, world, port, splits, cases, d)) for g in range(world)]
+        procs = [ctx.Process(target=target, args=args(g, d)) for g in range(world)]
         for p in procs:
             p.start()
         for p in procs:
@@ -56,7 +58,8 @@ def _run_world(world: int, splits, cases, timeout: float = 900):
                 out.append(json.load(f))
     for r in out:
         assert r["error"] is None, f"rank {r['rank']}:\n{r['error']}"
-        assert len(r["checks"]) == len(splits) * len(cases)
+        if fn == "run":
+            assert len(r["checks"]) == len(splits) * len(cases)
     return out
 
 
@@ -69,3 +72,25 @@ def test_peer_transport_toy_2x2_config0():
     """BASELINE.json configs[0]: toy DiT attention, B=1, H=4, D=64, 1024 tokens, Ulysses=2 x Ring=2,
     four real processes, against the unsplit fp64 oracle."""
     _run_world(4, [(2, 2)], [(1, 4, 0, 1024, 64, "bf16", True)])
+
+
+# (B, S_txt, S_img, H, D, L, T, M, warmup, dtype): PipeFusion stages as processes (NEXT 3)
+PF_CASES = [(1, 9, 300, 2, 64, 4, 3, 4, 1, "f32"), (2, 0, 256, 2, 128, 4, 4, 4, 2, "bf16"),
+            (1, 16, 400, 2, 72, 8, 3, 8, 1, "bf16")]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_pipefusion_stage_processes(world):
+    """One PipeFusion stage per process, patch activations and eps moved by the peer transport's
+    mailbox ("asynchronous P2P"): stage 0's latent equals the in-process schedule bit for bit
+    and the fp64 staleness oracle within the NEXT 3 gates."""
+    out = _run_world(world, None, PF_CASES, fn="run_pipefusion")
+    assert len(out[0]["checks"]) == len(PF_CASES)
+
+
+def test_cfg_tail_peer_transport():
+    """NEXT 2 over the peer transport: the two CFG branches gathered through the mailbox and
+    combined on both ranks, twice (the ack protocol), against oracle.cfg_combine."""
+    cases = [(4096, "bf16", 4.5), (4096, "f32", 7.5), (64, "bf16", 0.0), (64, "f32", 1.0)]
+    out = _run_world(2, None, cases, fn="run_cfg_tail")
+    assert all(len(r["checks"]) == len(cases) for r in out)
