@@ -379,6 +379,25 @@ XDIT_API int xdit_pf_block(void* h, void* kv_buf, const float* w, void* work, si
  * buffers of dtype 0 (bf16) or 1 (fp32); fp32 math, one rounding.  Errors: INVALID_ARG, ALIGNMENT, CUDA. */
 XDIT_API int xdit_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype, xdit_stream_t stream);
 
+/* ------------------------------------------------------------------------------------------ */
+/* patch-parallel VAE decode (§4.3; reading R5). */
+/* Devices hold row bands of the feature maps; before every conv a band receives one boundary row  */
+/* from each neighbour ("the exchange of the boundary data for convolutional operators";    */
+/* paper_2411_01738_b200/vae.py moves them through the peer-transport mailbox), so activation       */
+/* memory per device falls to ~1/N and the decode stays exact.                              */
+/* ------------------------------------------------------------------------------------------ */
+
+/* One decoder conv on a row band: out = conv3x3(in) + b, zero padding in x only.
+ * in   : DEVICE fp32 [H+2][Ci][W] -- the band's H rows with its top and bottom halo rows (zeros at
+ *        the image edges, which is the serial conv's zero padding)
+ * w, b : DEVICE fp32 [Co][Ci][3][3] (16-byte aligned), [Co]
+ * out  : DEVICE fp32 [H][Co][W], or with act_up = 1 (a decoder stage) SiLU then nearest x2 upsample,
+ *        [2H][Co][2W]
+ * Each output pixel is summed in one fixed order, so a band produces exactly the pixels of the
+ * whole-image call.  Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_vae_conv3x3(const float* in, int H, int Ci, int W, const float* w, const float* b, float* out,
+                              int Co, int act_up, xdit_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1077,6 +1077,17 @@ int xdit_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype,
   return XDIT_OK;
 }
 
+int xdit_vae_conv3x3(const float* in, int H, int Ci, int W, const float* w, const float* b, float* out, int Co,
+                     int act_up, xdit_stream_t stream) {
+  if (!in || !w || !b || !out) return fail(XDIT_ERR_INVALID_ARG, "xdit_vae_conv3x3: NULL pointer");
+  if (H < 0 || Ci < 1 || W < 0 || Co < 1 || (act_up != 0 && act_up != 1))
+    return fail(XDIT_ERR_INVALID_ARG, "xdit_vae_conv3x3: bad sizes (H=%d Ci=%d W=%d Co=%d act_up=%d)", H, Ci, W, Co,
+                act_up);
+  if (!aligned16(w)) return fail(XDIT_ERR_ALIGNMENT, "xdit_vae_conv3x3: weights must be 16-byte aligned");
+  XCUDA(xdit::launch_vae_conv3x3(in, H, Ci, W, w, b, out, Co, act_up, reinterpret_cast<cudaStream_t>(stream)));
+  return XDIT_OK;
+}
+
 int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,
                   int Sq, int Skv, int D, int64_t q_b, int64_t q_s, int64_t q_h, int64_t kv_b,
                   int64_t kv_s, int64_t kv_h, const xdit_rowmap* omap, int dtype, int out_f32,

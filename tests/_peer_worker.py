@@ -168,3 +168,50 @@ def run_cfg_tail(rank: int, world: int, port: int, cases, out_dir: str):
         res["error"] = traceback.format_exc()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump(res, f)
+
+
+def run_vae(rank: int, world: int, port: int, cases, out_dir: str):
+    """Patch-parallel VAE decode, one process per row band (paper_2411_01738_b200.vae.decode_band):
+    each band equals the same rows of the one-device GPU decode bit for bit and of the fp64 oracle."""
+    res = {"rank": rank, "checks": [], "error": None}
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        from oracle import vae as ovae
+        from paper_2411_01738_b200 import usp, vae
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        comm = usp.Comm(world, 1, transport="peer")
+        for ci, (h, c, w, widths) in enumerate(cases):
+            rng = np.random.default_rng(80 + ci)
+            lat = rng.standard_normal((h, c, w)).astype(np.float32)
+            L, cin = [], c
+            for co in list(widths) + [3]:
+                L.append(((rng.standard_normal((co, cin, 3, 3)) / np.sqrt(9 * cin)).astype(np.float32),
+                          (rng.standard_normal(co) * 0.1).astype(np.float32)))
+                cin = co
+            dec = vae.Decoder(L)
+            o, n = vae.bands(h, world)[rank]
+            mine = vae.decode_band(torch.from_numpy(lat[o:o + n]).cuda(), dec, comm)
+            whole = vae.decode(torch.from_numpy(lat).cuda(), dec)
+            torch.cuda.synchronize()
+            up = 2 ** len(widths)
+            assert torch.equal(mine, whole[o * up:(o + n) * up]), "band differs from the one-device decode"
+            want = ovae.serial_decode(lat, [(a.astype(np.float64), b.astype(np.float64)) for a, b in L])
+            err = float(np.abs(mine.cpu().double().numpy() - want[o * up:(o + n) * up]).max() / np.abs(want).max())
+            assert err <= 1e-5, err
+            res["checks"].append({"case": ci, "err": err, "band_rows": int(mine.shape[0])})
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        res["error"] = traceback.format_exc()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(res, f)

@@ -94,3 +94,12 @@ def test_cfg_tail_peer_transport():
     cases = [(4096, "bf16", 4.5), (4096, "f32", 7.5), (64, "bf16", 0.0), (64, "f32", 1.0)]
     out = _run_world(2, None, cases, fn="run_cfg_tail")
     assert all(len(r["checks"]) == len(cases) for r in out)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_vae_band_processes(world):
+    """NEXT 4: one process per latent row band, halo rows exchanged through the mailbox before
+    every conv: each band is bit-identical to the one-device decode and matches the oracle."""
+    cases = [(16, 4, 24, (32, 16)), (13, 16, 9, (64,))]
+    out = _run_world(world, None, cases, fn="run_vae")
+    assert all(len(r["checks"]) == len(cases) for r in out)
