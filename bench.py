@@ -166,6 +166,22 @@ def oracle_sample(w, seconds: float, rank_seed: int = 0):
     return n * per_row / dt, cores, desc, dt
 
 
+def ours_config(args, w):
+    """The `config` object our arm prints for the same launch (so both lines name one workload)."""
+    N = args.gpus
+    cfg, u, r = default_split(N, w.H, w.cfg)
+    if args.ulysses or args.ring:
+        u = args.ulysses or max(1, N // cfg // max(1, args.ring))
+        r = args.ring or max(1, N // cfg // u)
+    sp = u * r
+    B = w.B * w.cfg // cfg
+    L = w.S // sp + (1 if w.S % sp else 0)
+    flush = 4 * B * L * w.H * w.D * 2 < 2 * L2_BYTES
+    return {"workload": w.name, "B": w.B * w.cfg, "H": w.H, "D": w.D, "S_txt": w.S_txt, "S_img": w.S_img,
+            "cfg": cfg, "ulysses": u, "ring": r, "transport": args.transport if sp > 1 else None,
+            "l2": "flushed between steps" if flush else "inputs larger than L2"}
+
+
 def run_reference(args, w, rank: int):
     if rank != 0:
         return 0
@@ -182,8 +198,7 @@ def run_reference(args, w, rank: int):
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": flops_step / rate * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": w.name, "B": w.B * w.cfg, "H": w.H, "D": w.D,
-                                        "S_txt": w.S_txt, "S_img": w.S_img},
+        "data": "synthetic", "config": ours_config(args, w),
         "cpu_baseline": {"value": tflops, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
         "e2e": {"value": tflops, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
