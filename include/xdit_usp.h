@@ -287,6 +287,13 @@ typedef struct xdit_rowmap {
   int32_t seg_off[9];
   int64_t o_seg, o_b, o_s, o_h;
   int64_t l_seg, l_b, l_h;
+  /* seg_table != 0: segment s starts at element o_seg_off[s] (O) / l_seg_off[s] (LSE) from the base
+   * pointer instead of s*o_seg / s*l_seg -- the peer transport points each segment at its owner's
+   * receive buffer (any address of the flat device address space, e.g. an NVLink peer mapping), so
+   * the epilogue's stores ARE the reverse all-to-all. */
+  int64_t o_seg_off[8];
+  int64_t l_seg_off[8];
+  int32_t seg_table;
 } xdit_rowmap;
 
 /* Flash attention forward of one (Q block, KV block) pair -- SURVEY §8(a) step a6.

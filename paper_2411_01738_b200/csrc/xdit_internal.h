@@ -87,8 +87,8 @@ __host__ __device__ inline RowDst rowmap_dst(const xdit_rowmap& m, int b, int ro
     if (i < m.nseg && row >= m.seg_off[i]) s = i;
   const int64_t r = row - m.seg_off[s];
   RowDst d;
-  d.o_off = s * m.o_seg + b * m.o_b + r * m.o_s + h * m.o_h;
-  d.l_off = s * m.l_seg + b * m.l_b + h * m.l_h + r;
+  d.o_off = (m.seg_table ? m.o_seg_off[s] : s * m.o_seg) + b * m.o_b + r * m.o_s + h * m.o_h;
+  d.l_off = (m.seg_table ? m.l_seg_off[s] : s * m.l_seg) + b * m.l_b + h * m.l_h + r;
   return d;
 }
 

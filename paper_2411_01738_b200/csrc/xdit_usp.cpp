@@ -197,6 +197,10 @@ int check_map_align(const xdit_rowmap* m, int vec_elems) {
   for (int64_t x : v)
     if (x % vec_elems != 0)
       return fail(XDIT_ERR_ALIGNMENT, "output strides must be multiples of %d elements", vec_elems);
+  if (m->seg_table)
+    for (int s = 0; s < m->nseg && s < 8; ++s)
+      if (m->o_seg_off[s] % vec_elems != 0)
+        return fail(XDIT_ERR_ALIGNMENT, "segment offsets must be multiples of %d elements", vec_elems);
   return XDIT_OK;
 }
 
@@ -501,6 +505,17 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     fmap.l_seg = int64_t(need.ochunk / 4);
     fmap.l_b = int64_t(Hh) * P.Lmax;
     fmap.l_h = P.Lmax;
+    if (peer) {  // a9 fused into the epilogue: segment p is stored straight into peer p's O receive
+                 // buffer at this rank's chunk (P.j); the final kernel's stores are the all-to-all
+      fmap.seg_table = 1;
+      const char* ob = static_cast<const char*>(dst);
+      const char* lb = reinterpret_cast<const char*>(dst_lse);
+      for (int p = 0; p < P.u; ++p) {
+        const char* chunk = static_cast<const char*>(c->peer[i * P.u + p].ptr[kHORecv]) + size_t(P.j) * need.ochunk;
+        fmap.o_seg_off[p] = (chunk - ob) / eb;
+        fmap.l_seg_off[p] = (chunk + need.ochunk_o - lb) / 4;
+      }
+    }
   }
 
   AttnArgs a{};
@@ -591,11 +606,7 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
 
   // ---- a9-a10: reverse all-to-all of O (+ LSE) and unpack into the caller's layout
   if (P.u > 1) {
-    if (peer) {  // chunk p (O rows + LSE of peer p's tokens) -> peer p's receive buffer at chunk P.j
-      for (int p = 0; p < P.u; ++p)
-        XCUDA(cudaMemcpyAsync(static_cast<char*>(c->peer[i * P.u + p].ptr[kHORecv]) + size_t(P.j) * need.ochunk,
-                              static_cast<const char*>(c->osend.p) + size_t(p) * need.ochunk, need.ochunk,
-                              cudaMemcpyDefault, st));
+    if (peer) {  // the final epilogue already stored chunk p in peer p's receive buffer: flag, wait
       for (int p = 0; p < P.u; ++p)
         if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFO + P.j, e));
       for (int p = 0; p < P.u; ++p)

@@ -32,7 +32,8 @@ class RowMap(ctypes.Structure):
     _fields_ = [("nseg", ctypes.c_int32), ("seg_off", ctypes.c_int32 * 9),
                 ("o_seg", ctypes.c_int64), ("o_b", ctypes.c_int64), ("o_s", ctypes.c_int64),
                 ("o_h", ctypes.c_int64), ("l_seg", ctypes.c_int64), ("l_b", ctypes.c_int64),
-                ("l_h", ctypes.c_int64)]
+                ("l_h", ctypes.c_int64), ("o_seg_off", ctypes.c_int64 * 8), ("l_seg_off", ctypes.c_int64 * 8),
+                ("seg_table", ctypes.c_int32)]
 
     @classmethod
     def plain(cls, B: int, S: int, H: int, D: int) -> "RowMap":
