@@ -182,6 +182,21 @@ def ours_config(args, w):
             "l2": "flushed between steps" if flush else "inputs larger than L2"}
 
 
+def comm_summary(pl, B: int, w, u: int, r: int, ms: float):
+    """Algorithmic bytes this rank sends per call (Table 1): the Ulysses
+    Q,K,V exchange and the O (+LSE) return to the u-1 peers, and r-1 ring steps of K,V; and the time
+    they take at NVLink 5's 900 GB/s per direction -- the share of the call a perfectly overlapped
+    transport would need (the Ulysses part is not overlapped)."""
+    if u * r == 1:
+        return None
+    a2a = (u - 1) * pl.a2a_bytes_per_peer  # Q, K, V to the u-1 peers
+    o_ret = (u - 1) * (B * pl.Lmax * pl.Hh * w.D * 2 + B * pl.Hh * pl.Lmax * 4) if u > 1 else 0
+    ring = sum(pl.ring_bytes[s] for s in range(r))
+    tot = a2a + o_ret + ring
+    return {"bytes_per_rank": int(tot), "ulysses_bytes": int(a2a + o_ret), "ring_bytes": int(ring),
+            "ms_at_900GBps": tot / 900e9 * 1e3, "share_of_call_at_900GBps": tot / 900e9 * 1e3 / ms}
+
+
 def run_reference(args, w, rank: int):
     if rank != 0:
         return 0
@@ -447,6 +462,7 @@ def main():
                     "serial": {"value": flops / (e2e_serial_ms * 1e-3) / 1e12, "ms_per_step": e2e_serial_ms,
                                "mode": "H2D, call, D2H back to back on one stream"}},
             "gpu_launches": int(launches),
+            "comm": comm_summary(pl, B, w, u, r, ms),
             "roofline": {"bound": "tensor", "kernel": attn_kernel_name(w.D), "achieved": kern_tflops,
                          "peak": peak, "unit": "TFLOP/s", "frac": kern_tflops / peak, "traffic": traffic,
                          "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
