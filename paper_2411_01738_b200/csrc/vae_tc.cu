@@ -1,0 +1,165 @@
+// vae_tc.cu -- SURVEY §8(f) NEXT 4 on the tensor cores: the decoder's 3x3 conv as an implicit GEMM
+// on tcgen05 (§4.3; reading R5, §7.7).
+//
+// out[y][x][co] = b[co] + sum_{dy,dx} sum_ci w[co][ci][dy][dx] * in[y+dy][x+dx-1][ci]
+// over a halo-extended row band in[H+2][W][Ci] (bf16, channels innermost), zero padding in x.
+// GEMM view per (tap, 64-channel chunk): A = 128 consecutive pixels of one input row, shifted by the
+// tap (TMA box (64 ch, 128 px) at (ci0, row y+dy, x0+dx-1); out-of-range pixels and channels are
+// zero-filled by the TMA, which IS the zero padding), B = the tap's weights for 128 output channels
+// (wt[9][Co][Ci], K-major), D = 128 pixels x 128 channels in TMEM (fp32), accumulated over 9 taps x
+// ceil(Ci/64) chunks, 4 MMAs (K = 16) each.  One CTA per (output row, 128-pixel strip, 128-channel
+// block); warp 4 = TMA producer, warp 5 = MMA issuer, warps 0-3 = epilogue (thread = pixel = TMEM
+// lane): bias, optional SiLU + nearest x2 upsample, bf16 store [H'][W'][Co].
+// Every pixel's sum is the same MMA sequence whatever band it sits in, so the banded decode stays
+// bit-identical to the whole-image decode.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "attn_common.cuh"
+
+namespace xdit {
+namespace {
+
+constexpr int kPix = 128, kCoT = 128, kKC = 64, kStages = 3;  // 3 stages: 2 CTAs per SM (one's epilogue overlaps the other's K loop)
+constexpr int kTileA = kPix * kKC * 2, kTileB = kCoT * kKC * 2;  // 16 KB each
+constexpr int kStageBytes = kTileA + kTileB;
+constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+
+__global__ void __launch_bounds__(192, 2)
+    vae_conv_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
+                       const float* __restrict__ bias, __nv_bfloat16* __restrict__ out, int Hout, int W, int Ci,
+                       int Co, int act_up) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* acc_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int x0 = blockIdx.x * kPix, y = blockIdx.y, co0 = blockIdx.z * kCoT;
+  const int nkc = (Ci + kKC - 1) / kKC, nk = 9 * nkc;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      ptx::mbar_init(&full[s], 1);
+      ptx::mbar_init(&empty[s], 1);
+    }
+    ptx::mbar_init(acc_full, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 5) {
+    ptx::tmem_alloc(tmem_slot, 128);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (warp == 4) {  // ---------------------------------------------------- TMA producer
+    if (lane == 0) {
+      ptx::tma_prefetch_desc(&tmX);
+      ptx::tma_prefetch_desc(&tmW);
+      const uint64_t pol_x = ptx::policy_evict_last(), pol_w = ptx::policy_evict_last();
+      for (int it = 0; it < nk; ++it) {
+        const int s = it % kStages, round = it / kStages;
+        if (round > 0) ptx::mbar_wait(&empty[s], (round - 1) & 1);
+        const int tap = it / nkc, c0 = (it % nkc) * kKC, dy = tap / 3, dx = tap % 3;
+        ptx::mbar_expect_tx(&full[s], kStageBytes);
+        uint8_t* st = smem + s * kStageBytes;
+        ptx::tma_load_4d(st, &tmX, &full[s], c0, y + dy, x0 + dx - 1, 0, pol_x);  // (ch, row, px)
+        ptx::tma_load_4d(st + kTileA, &tmW, &full[s], c0, tap, co0, 0, pol_w);  // (ci, tap, co)
+      }
+    }
+  } else if (warp == 5) {  // -------------------------------------------- MMA issuer
+    constexpr uint32_t idesc = ptx::idesc_bf16_f32(kPix, kCoT, 0, 0);
+    const uint32_t sa = ptx::smem_u32(smem);
+    for (int it = 0; it < nk; ++it) {
+      const int s = it % kStages;
+      ptx::mbar_wait(&full[s], (it / kStages) & 1);
+      ptx::tc_fence_after();
+      if (ptx::elect_one()) {
+        const uint32_t a = sa + s * kStageBytes, b = a + kTileA;
+#pragma unroll
+        for (int k = 0; k < kKC / 16; ++k)
+          ptx::mma_ss(tmem, ptx::sdesc_sw128(a + k * 32, 16, 1024), ptx::sdesc_sw128(b + k * 32, 16, 1024), idesc,
+                      (it > 0 || k > 0) ? 1u : 0u);
+        ptx::tc_commit(&empty[s]);
+        if (it == nk - 1) ptx::tc_commit(acc_full);
+      }
+      __syncwarp();
+    }
+  } else {  // ------------------------------------------------------------ epilogue (warps 0-3)
+    ptx::mbar_wait_sleep(acc_full, 0);  // the whole K loop: sleep instead of polling
+    ptx::tc_fence_after();
+    const int x = x0 + warp * 32 + lane;
+    const uint32_t tl = tmem + (uint32_t(warp * 32) << 16);
+#pragma unroll 1
+    for (int cb = 0; cb < kCoT; cb += 32) {
+      uint32_t r[32];
+      ptx::tmem_ld32(tl + cb, r);
+      ptx::tmem_ld_wait();
+      if (x >= W) continue;
+      float v[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int co = co0 + cb + i;
+        v[i] = u2f(r[i]) + (co < Co ? bias[co] : 0.f);
+        if (act_up) v[i] = v[i] / (1.f + expf(-v[i]));
+      }
+      const int nco = min(32, Co - (co0 + cb));
+      if (nco <= 0) continue;
+      auto store = [&](int yy, int xx, int Wd) {
+        __nv_bfloat16* o = out + (int64_t(yy) * Wd + xx) * Co + co0 + cb;
+        if (nco == 32 && (Co % 8) == 0) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            reinterpret_cast<uint4*>(o)[q] =
+                make_uint4(ptx::pack_bf16x2(v[8 * q], v[8 * q + 1]), ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+                           ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (i < nco) o[i] = __float2bfloat16_rn(v[i]);
+        }
+      };
+      if (act_up) {
+        store(2 * y, 2 * x, 2 * W);
+        store(2 * y, 2 * x + 1, 2 * W);
+        store(2 * y + 1, 2 * x, 2 * W);
+        store(2 * y + 1, 2 * x + 1, 2 * W);
+      } else {
+        store(y, x, W);
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 5) ptx::tmem_dealloc(tmem, 128);
+}
+
+}  // namespace
+
+cudaError_t launch_vae_conv_tc(const void* in, int Hout, int Ci, int W, const void* wt, const float* b, void* out,
+                               int Co, int act_up, cudaStream_t st) {
+  if (Hout == 0 || W == 0) return cudaSuccess;
+  CUtensorMap mx, mw;
+  // activations [Hout+2][W][Ci]: dims (Ci, rows->"H", pixels->"S"); box 64 channels x 128 pixels
+  if (!make_map(&mx, in, 1, W, Hout + 2, Ci, int64_t(Hout + 2) * W * Ci, Ci, int64_t(W) * Ci, kKC, kPix) ||
+      !make_map(&mw, wt, 1, Co, 9, Ci, int64_t(9) * Co * Ci, Ci, int64_t(Co) * Ci, kKC, kCoT))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(vae_conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid((W + kPix - 1) / kPix, Hout, (Co + kCoT - 1) / kCoT);
+  vae_conv_tc_kernel<<<grid, 192, kSmem, st>>>(mx, mw, b, static_cast<__nv_bfloat16*>(out), Hout, W, Ci, Co, act_up);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+}  // namespace xdit

@@ -72,6 +72,8 @@ cudaError_t launch_pf_sampler(void* x, const void* eps, int64_t n, float sigma, 
 // SURVEY §8(f) NEXT 4, patch-parallel VAE decode (vae.cu).
 cudaError_t launch_vae_conv3x3(const float* in, int Hout, int Ci, int W, const float* w, const float* b, float* out,
                                int Co, int act_up, cudaStream_t st);
+cudaError_t launch_vae_conv_tc(const void* in, int Hout, int Ci, int W, const void* wt, const float* b, void* out,
+                               int Co, int act_up, cudaStream_t st);
 
 // Device-side row-map resolution shared by every epilogue that writes through an xdit_rowmap.
 struct RowDst {

@@ -1099,6 +1099,19 @@ int xdit_vae_conv3x3(const float* in, int H, int Ci, int W, const float* w, cons
   return XDIT_OK;
 }
 
+int xdit_vae_conv3x3_bf16(const void* in, int H, int Ci, int W, const void* wt, const float* b, void* out, int Co,
+                          int act_up, xdit_stream_t stream) {
+  if (!in || !wt || !b || !out) return fail(XDIT_ERR_INVALID_ARG, "xdit_vae_conv3x3_bf16: NULL pointer");
+  if (H < 0 || Ci < 1 || W < 0 || Co < 1 || (act_up != 0 && act_up != 1))
+    return fail(XDIT_ERR_INVALID_ARG, "xdit_vae_conv3x3_bf16: bad sizes (H=%d Ci=%d W=%d Co=%d act_up=%d)", H, Ci, W,
+                Co, act_up);
+  if (Ci % 8 || !aligned16(in) || !aligned16(wt) || !aligned16(out))
+    return fail(XDIT_ERR_ALIGNMENT, "xdit_vae_conv3x3_bf16: Ci %% 8 == 0 and 16-byte aligned pointers required");
+  const cudaError_t e = xdit::launch_vae_conv_tc(in, H, Ci, W, wt, b, out, Co, act_up, reinterpret_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return fail(XDIT_ERR_CUDA, "vae conv (tcgen05) launch failed: %s", cudaGetErrorString(e));
+  return XDIT_OK;
+}
+
 int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,
                   int Sq, int Skv, int D, int64_t q_b, int64_t q_s, int64_t q_h, int64_t kv_b,
                   int64_t kv_s, int64_t kv_h, const xdit_rowmap* omap, int dtype, int out_f32,

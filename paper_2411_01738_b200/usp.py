@@ -99,6 +99,7 @@ _SIGS = {
     "xdit_pf_block": ([_vp] * 4 + [ctypes.c_size_t] + [_i] * 7 + [_vp], _i),
     "xdit_pf_sampler": ([_vp, _vp, _i64, ctypes.c_float, _i, _vp], _i),
     "xdit_vae_conv3x3": ([_vp, _i, _i, _i, _vp, _vp, _vp, _i, _i, _vp], _i),
+    "xdit_vae_conv3x3_bf16": ([_vp, _i, _i, _i, _vp, _vp, _vp, _i, _i, _vp], _i),
 }
 
 

@@ -1,9 +1,11 @@
 """Patch-parallel VAE decode -- SURVEY §8(f) NEXT 4 (§4.3; reading R5).
 
-Host orchestration only: every conv runs in the library's `xdit_vae_conv3x3` (conv + bias, the
-stage's SiLU and x2 upsample fused into the store); halo rows move between devices through the
-peer-transport mailbox.  Activations are fp32 [H][C][W].  The decoder: per stage a 3x3 conv + SiLU +
-nearest x2 upsample, then a final 3x3 conv to 3 channels.
+Host orchestration only: every conv runs in the library -- `xdit_vae_conv3x3` (SIMT fp32,
+activations [H][C][W]) or, with tc=True, `xdit_vae_conv3x3_bf16` (tcgen05 implicit GEMM, bf16
+activations [H][W][C], channels padded to a multiple of 8) -- with the stage's SiLU and x2 upsample
+fused into the store; halo rows move between devices through the peer-transport mailbox.  In both
+layouts a row of the feature map is contiguous.  The decoder: per stage a 3x3 conv + SiLU + nearest
+x2 upsample, then a final 3x3 conv to 3 channels.
 """
 from __future__ import annotations
 
@@ -25,18 +27,56 @@ def bands(h: int, N: int) -> List[Tuple[int, int]]:
     return out
 
 
-class Decoder:
-    """layers: [(w [Co][Ci][3][3], b [Co])]; all but the last are upsampling stages."""
+def _pad8(n: int) -> int:
+    return (n + 7) // 8 * 8
 
-    def __init__(self, layers: Sequence, device="cuda"):
+
+class Decoder:
+    """layers: [(w [Co][Ci][3][3], b [Co])]; all but the last are upsampling stages.
+    tc=False: fp32 weights as given (SIMT kernel); tc=True: bf16 tap-major weights [9][Co][Ci'] with
+    Ci' = Ci rounded up to a multiple of 8 (zero rows: exact), for the tcgen05 kernel."""
+
+    def __init__(self, layers: Sequence, device="cuda", tc: bool = False):
         import torch
-        self.layers = [(torch.as_tensor(w, dtype=torch.float32).contiguous().to(device),
-                        torch.as_tensor(b, dtype=torch.float32).contiguous().to(device)) for w, b in layers]
+        self.tc = tc
+        self.layers = []
+        for w, b in layers:
+            w = torch.as_tensor(w, dtype=torch.float32)
+            b = torch.as_tensor(b, dtype=torch.float32).contiguous().to(device)
+            if tc:
+                Co, Ci = w.shape[:2]
+                wt = torch.zeros(9, Co, _pad8(Ci))
+                wt[:, :, :Ci] = w.permute(2, 3, 0, 1).reshape(9, Co, Ci)
+                w = wt.to(torch.bfloat16)
+            self.layers.append((w.contiguous().to(device), b))
+
+    def prepare(self, latent):
+        """The latent in this decoder's layout: fp32 [h][c][w] as given, or for tc bf16 [h][w][c'] with
+        zero channels up to c' (a multiple of 8)."""
+        import torch
+        if not self.tc:
+            return latent
+        h, c, w = latent.shape
+        x = torch.zeros((h, w, _pad8(c)), dtype=torch.bfloat16, device=latent.device)
+        x[:, :, :c] = latent.permute(0, 2, 1)
+        return x
 
 
 def conv(ext, w, b, act_up: bool, stream=None):
-    """xdit_vae_conv3x3 on a halo-extended band ext [H+2][Ci][W]; returns the new band."""
+    """One decoder conv on a halo-extended band: fp32 ext [H+2][Ci][W] with w [Co][Ci][3][3]
+    (xdit_vae_conv3x3), or bf16 ext [H+2][W][Ci] with tap-major w [9][Co][Ci] (xdit_vae_conv3x3_bf16)."""
     import torch
+    if ext.dtype == torch.bfloat16:
+        Hp2, W, Ci = ext.shape
+        H, Co = Hp2 - 2, w.shape[1]
+        out = torch.empty((2 * H, 2 * W, Co) if act_up else (H, W, Co), dtype=torch.bfloat16, device=ext.device)
+        usp._check(usp.lib().xdit_vae_conv3x3_bf16(usp._ptr(ext), H, Ci, W, usp._ptr(w), usp._ptr(b), usp._ptr(out),
+                                                   Co, 1 if act_up else 0, usp._stream(stream)), "xdit_vae_conv3x3_bf16")
+        if Co % 8 and act_up:  # the next conv needs Ci % 8 == 0 (TMA row stride): zero channels
+            pad = torch.zeros(out.shape[:2] + (_pad8(Co),), dtype=out.dtype, device=out.device)
+            pad[:, :, :Co] = out
+            out = pad
+        return out
     Hp2, Ci, W = ext.shape
     H, Co = Hp2 - 2, w.shape[0]
     out = torch.empty((2 * H, Co, 2 * W) if act_up else (H, Co, W), dtype=torch.float32, device=ext.device)
@@ -46,11 +86,12 @@ def conv(ext, w, b, act_up: bool, stream=None):
 
 
 def decode(latent, dec: Decoder):
-    """Single-device decode: the whole image is one band with zero halo rows."""
+    """Single-device decode: the whole image is one band with zero halo rows.  latent: fp32 [h][c][w]
+    (SIMT decoder) or already in the tc decoder's layout (Decoder.prepare)."""
     import torch
     x = latent
     for i, (w, b) in enumerate(dec.layers):
-        ext = torch.zeros((x.shape[0] + 2,) + tuple(x.shape[1:]), dtype=torch.float32, device=x.device)
+        ext = torch.zeros((x.shape[0] + 2,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         ext[1:-1].copy_(x)
         x = conv(ext, w, b, i < len(dec.layers) - 1)
     return x
@@ -58,26 +99,27 @@ def decode(latent, dec: Decoder):
 
 def decode_band(band, dec: Decoder, comm):
     """Patch-parallel decode, one process per band: this rank (= comm.rank of N) holds latent rows
-    `band` [h_g][c][w]; before every conv it sends its first row to rank g-1 and its last row to rank
+    `band` ([h_g][c][w] fp32, or [h_g][w][c'] bf16 for a tc decoder); two mailbox spaces (layer
+    parity) per source hold the halo rows; before every conv it sends its first row to rank g-1 and its last row to rank
     g+1 (their bottom / top halos) through the mailbox and receives theirs.  Collective.  Returns
     this rank's band of the decoded image."""
     import torch
     N, g = comm.ulysses * comm.ring, comm.rank
     st = torch.cuda.current_stream()
-    # halo row bytes of the widest layer input, two spaces (layer parity) per source
+    # a row of the widest layer input ([C][W] fp32 or [W][C'] bf16; the upsampling doubles W)
+    C, W = (band.shape[2], band.shape[1]) if dec.tc else (band.shape[1], band.shape[2])
     rows = []
-    C, W = band.shape[1], band.shape[2]
     for i, (w, _) in enumerate(dec.layers):
-        rows.append(C * W * 4)
-        C = w.shape[0]
-        W = W * 2 if i < len(dec.layers) - 1 else W
+        rows.append(C * W * band.element_size())
+        C = _pad8(w.shape[1]) if dec.tc else w.shape[0]
+        W = 2 * W if i < len(dec.layers) - 1 else W
     rb = (max(rows) + 255) // 256 * 256
     comm.mailbox(2 * rb)
     tags = comm.__dict__.setdefault("_vae_tags", {})
     x = band
     for i, (w, b) in enumerate(dec.layers):
         h = x.shape[0]
-        ext = torch.empty((h + 2,) + tuple(x.shape[1:]), dtype=torch.float32, device=x.device)
+        ext = torch.empty((h + 2,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         ext[1:-1].copy_(x)
         for nb, row in ((g - 1, x[0]), (g + 1, x[h - 1])):  # my boundary rows -> the neighbours
             if 0 <= nb < N:
@@ -89,7 +131,7 @@ def decode_band(band, dec: Decoder, comm):
             if 0 <= nb < N:
                 t = tags[("in", nb)] = tags.get(("in", nb), 0) + 1
                 comm.wait(nb, t, stream=st)
-                dst.copy_(comm.mailbox_view(nb, tuple(dst.shape), torch.float32, offset=(t % 2) * rb))
+                dst.copy_(comm.mailbox_view(nb, tuple(dst.shape), x.dtype, offset=(t % 2) * rb))
                 comm.ack(nb, t, stream=st)
             else:
                 dst.zero_()

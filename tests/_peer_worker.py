@@ -187,7 +187,7 @@ def run_vae(rank: int, world: int, port: int, cases, out_dir: str):
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
         comm = usp.Comm(world, 1, transport="peer")
-        for ci, (h, c, w, widths) in enumerate(cases):
+        for ci, (h, c, w, widths, tc) in enumerate(cases):
             rng = np.random.default_rng(80 + ci)
             lat = rng.standard_normal((h, c, w)).astype(np.float32)
             L, cin = [], c
@@ -195,16 +195,23 @@ def run_vae(rank: int, world: int, port: int, cases, out_dir: str):
                 L.append(((rng.standard_normal((co, cin, 3, 3)) / np.sqrt(9 * cin)).astype(np.float32),
                           (rng.standard_normal(co) * 0.1).astype(np.float32)))
                 cin = co
-            dec = vae.Decoder(L)
+            dec = vae.Decoder(L, tc=tc)
             o, n = vae.bands(h, world)[rank]
-            mine = vae.decode_band(torch.from_numpy(lat[o:o + n]).cuda(), dec, comm)
-            whole = vae.decode(torch.from_numpy(lat).cuda(), dec)
+            x0 = dec.prepare(torch.from_numpy(lat).cuda())
+            mine = vae.decode_band(x0[o:o + n].contiguous(), dec, comm)
+            whole = vae.decode(x0, dec)
             torch.cuda.synchronize()
             up = 2 ** len(widths)
             assert torch.equal(mine, whole[o * up:(o + n) * up]), "band differs from the one-device decode"
             want = ovae.serial_decode(lat, [(a.astype(np.float64), b.astype(np.float64)) for a, b in L])
-            err = float(np.abs(mine.cpu().double().numpy() - want[o * up:(o + n) * up]).max() / np.abs(want).max())
-            assert err <= 1e-5, err
+            want = want[o * up:(o + n) * up]
+            if tc:  # bf16 [H][W][C'] -> [H][C][W]
+                got = mine[:, :, :3].permute(0, 2, 1).double().cpu().numpy()
+                err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+                assert err <= 2e-2, err
+            else:
+                err = float(np.abs(mine.cpu().double().numpy() - want).max() / np.abs(want).max())
+                assert err <= 1e-5, err
             res["checks"].append({"case": ci, "err": err, "band_rows": int(mine.shape[0])})
         torch.cuda.synchronize()
         dist.barrier()

@@ -100,6 +100,6 @@ def test_cfg_tail_peer_transport():
 def test_vae_band_processes(world):
     """NEXT 4: one process per latent row band, halo rows exchanged through the mailbox before
     every conv: each band is bit-identical to the one-device decode and matches the oracle."""
-    cases = [(16, 4, 24, (32, 16)), (13, 16, 9, (64,))]
+    cases = [(16, 4, 24, (32, 16), False), (13, 16, 9, (64,), False), (12, 4, 140, (64, 32), True)]
     out = _run_world(world, None, cases, fn="run_vae")
     assert all(len(r["checks"]) == len(cases) for r in out)
