@@ -418,6 +418,15 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
                     need.kvslot);
     }
   }
+  if (peer) {
+    // the flag values are immediates of the stream memory operations: a captured call would replay
+    // the same epoch and its waits would pass on the previous replay's flags -- refuse capture
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    XCUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)
+      return fail(XDIT_ERR_UNSUPPORTED, "the peer transport cannot be captured in a CUDA graph (per-call epochs); "
+                  "use the NCCL transport or N = 1 for graphs");
+  }
   const uint32_t e = peer ? ++c->epoch : 0u;  // every rank issues the same calls: epochs agree
 
   const int i = P.i, Hh = P.Hh, L = P.S_loc[c->rank], Sb = P.S_blk[i];

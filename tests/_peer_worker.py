@@ -222,3 +222,45 @@ def run_vae(rank: int, world: int, port: int, cases, out_dir: str):
         res["error"] = traceback.format_exc()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump(res, f)
+
+
+def run_graph_refusal(rank: int, world: int, port: int, cases, out_dir: str):
+    """A peer-transport USP call inside CUDA-graph capture is refused (UNSUPPORTED), not mis-captured."""
+    res = {"rank": rank, "checks": [], "error": None}
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import torch
+        import torch.distributed as dist
+
+        from paper_2411_01738_b200 import usp
+        from paper_2411_01738_b200.inputs import qkv
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        comm = usp.Comm(world, 1, transport="peer")
+        q, k, v = (t[:, rank * 64:(rank + 1) * 64].contiguous().cuda() for t in qkv(1, 64 * world, 2 * world, 64, seed=1))
+        usp.attention(q, k, v, S_txt=0, S_img=64 * world, comm=comm, ulysses=world, ring=1)  # reserve + eager call
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        s = torch.cuda.Stream()
+        refused = False
+        with torch.cuda.stream(s):
+            try:
+                with torch.cuda.graph(g, stream=s):
+                    usp.attention(q, k, v, S_txt=0, S_img=64 * world, comm=comm, ulysses=world, ring=1)
+            except usp.XditError as e:
+                refused = e.status == "UNSUPPORTED"
+            except RuntimeError:
+                pass  # capture aborted by the raise inside it
+        assert refused, "capture of a peer-transport call was not refused"
+        res["checks"].append({"refused": True})
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        res["error"] = traceback.format_exc()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(res, f)

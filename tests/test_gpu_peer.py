@@ -103,3 +103,10 @@ def test_vae_band_processes(world):
     cases = [(16, 4, 24, (32, 16), False), (13, 16, 9, (64,), False), (12, 4, 140, (64, 32), True)]
     out = _run_world(world, None, cases, fn="run_vae")
     assert all(len(r["checks"]) == len(cases) for r in out)
+
+
+def test_peer_transport_refuses_graph_capture():
+    """The peer transport bakes per-call epochs into its stream operations, so a captured call could
+    not be replayed safely: capture is refused with XDIT_ERR_UNSUPPORTED (include/xdit_usp.h)."""
+    out = _run_world(2, None, None, fn="run_graph_refusal")
+    assert all(r["checks"] for r in out)
