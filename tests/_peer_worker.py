@@ -264,3 +264,55 @@ def run_graph_refusal(rank: int, world: int, port: int, cases, out_dir: str):
         res["error"] = traceback.format_exc()
     with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
         json.dump(res, f)
+
+
+def run_errors(rank: int, world: int, port: int, cases, out_dir: str):
+    """Peer-transport error paths (include/xdit_usp.h): a call after a reallocating reserve without
+    re-connecting -> NOT_CONNECTED; a mailbox message larger than the region -> WORKSPACE; the mesh
+    of the blobs must match the handle -> COMM_MISMATCH; nothing is enqueued on failure."""
+    res = {"rank": rank, "checks": [], "error": None}
+    try:
+        os.environ["MASTER_ADDR"] = "127.0.0.1"
+        os.environ["MASTER_PORT"] = str(port)
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+
+        from paper_2411_01738_b200 import usp
+
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        torch.cuda.set_device(0)
+        L = usp.lib()
+        comm = usp.Comm(world, 1, transport="peer")
+        comm.reserve(1, 2 * world, 0, 64 * world, 64, 2)
+        # grow the workspace behind the binding's back: the peers' mappings are stale now
+        torch.cuda.synchronize()
+        dist.barrier()
+        usp._check(L.xdit_comm_reserve(comm.handle, 1, 2 * world, 0, 4096 * world, 64, 2), "xdit_comm_reserve")
+        q = torch.zeros(1, 4096, 2 * world, 64, dtype=torch.bfloat16, device="cuda")
+        rc = L.xdit_usp_attention(usp._ptr(q), usp._ptr(q), usp._ptr(q), usp._ptr(q), None, 1, 2 * world, 0,
+                                  4096 * world, 64, world, 1, usp._stream(None), comm.handle)
+        assert usp.XDIT_STATUS[rc] == "NOT_CONNECTED", (rc, usp.last_error())
+        res["checks"].append("not_connected")
+        comm.mailbox(1024)
+        src = torch.zeros(4096, dtype=torch.uint8, device="cuda")
+        try:
+            comm.put((rank + 1) % world, src, 1)
+            raise AssertionError("oversized put was accepted")
+        except usp.XditError as e:
+            assert e.status == "WORKSPACE", e
+        res["checks"].append("workspace")
+        blob = (ctypes.c_uint8 * (usp.PEER_BLOB_BYTES * world))()
+        rc = L.xdit_comm_peer_connect(comm.handle, ctypes.cast(blob, ctypes.c_void_p))  # all-zero blobs
+        assert usp.XDIT_STATUS[rc] == "COMM_MISMATCH", (rc, usp.last_error())
+        res["checks"].append("mismatch")
+        torch.cuda.synchronize()
+        dist.barrier()
+        comm.destroy()
+        dist.barrier()
+        dist.destroy_process_group()
+    except Exception:
+        res["error"] = traceback.format_exc()
+    with open(os.path.join(out_dir, f"rank{rank}.json"), "w") as f:
+        json.dump(res, f)

@@ -110,3 +110,8 @@ def test_peer_transport_refuses_graph_capture():
     not be replayed safely: capture is refused with XDIT_ERR_UNSUPPORTED (include/xdit_usp.h)."""
     out = _run_world(2, None, None, fn="run_graph_refusal")
     assert all(r["checks"] for r in out)
+
+
+def test_peer_transport_error_paths():
+    out = _run_world(2, None, None, fn="run_errors")
+    assert all(r["checks"] == ["not_connected", "workspace", "mismatch"] for r in out)
