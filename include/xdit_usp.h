@@ -411,7 +411,8 @@ XDIT_API int xdit_vae_conv3x3(const float* in, int H, int Ci, int W, const float
  * DESIGN.md §7.7).  Channels-innermost layouts:
  * in   : DEVICE bf16 [H+2][W][Ci] (band + halo rows), Ci % 8 == 0
  * wt   : DEVICE bf16 [9][Co][Ci] (tap-major: wt[3*dy+dx][co][ci] = w[co][ci][dy][dx]);  b: fp32 [Co]
- * out  : DEVICE bf16 [H][W][Co], or with act_up = 1 SiLU + nearest x2 upsample, [2H][2W][Co]
+ * out  : DEVICE bf16 [H][W][Co8], or with act_up = 1 SiLU + nearest x2 upsample, [2H][2W][Co8];
+ *        Co8 = Co rounded up to a multiple of 8 (16-byte rows for the TMA stores), channels >= Co are 0
  * Each pixel's accumulation is the same MMA sequence in any band (bit-exact patch parallelism).
  * Errors: INVALID_ARG, ALIGNMENT, CUDA. */
 XDIT_API int xdit_vae_conv3x3_bf16(const void* in, int H, int Ci, int W, const void* wt, const float* b, void* out,

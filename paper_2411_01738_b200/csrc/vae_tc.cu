@@ -9,7 +9,8 @@
 // (wt[9][Co][Ci], K-major), D = 128 pixels x 128 channels in TMEM (fp32), accumulated over 9 taps x
 // ceil(Ci/64) chunks, 4 MMAs (K = 16) each.  One CTA per (output row, 128-pixel strip, 128-channel
 // block); warp 4 = TMA producer, warp 5 = MMA issuer, warps 0-3 = epilogue (thread = pixel = TMEM
-// lane): bias, optional SiLU + nearest x2 upsample, bf16 store [H'][W'][Co].
+// lane): bias, optional SiLU + nearest x2 upsample, bf16 [H'][W'][Co8] (Co rounded up to 8, the extra
+// channels zero) written through shared memory with TMA stores.
 // Every pixel's sum is the same MMA sequence whatever band it sits in, so the banded decode stays
 // bit-identical to the whole-image decode.
 #include <cuda.h>
@@ -29,12 +30,28 @@ constexpr int kTileA = kPix * kKC * 2, kTileB = kCoT * kKC * 2;  // 16 KB each
 constexpr int kStageBytes = kTileA + kTileB;
 constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
 
+// TMA store of a 4-D box from shared memory (bulk-group completion) and its helpers.
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2,
+                                             int c3) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(map)),
+               "r"(ptx::smem_u32(smem_src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
 __global__ void __launch_bounds__(192, 2)
     vae_conv_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
-                       const float* __restrict__ bias, __nv_bfloat16* __restrict__ out, int Hout, int W, int Ci,
-                       int Co, int act_up) {
+                       const __grid_constant__ CUtensorMap tmO, const float* __restrict__ bias, int Hout, int W,
+                       int Ci, int Co, int act_up) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // output staging (up to 256 pixels x 32 channels bf16 = 16 KB, 64B swizzle atoms): the operand
+  // stages are free once the last MMA has completed, so the epilogue reuses stage 0
+  uint8_t* stage_out = smem;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* acc_full = empty + kStages;
@@ -94,46 +111,53 @@ __global__ void __launch_bounds__(192, 2)
   } else {  // ------------------------------------------------------------ epilogue (warps 0-3)
     ptx::mbar_wait_sleep(acc_full, 0);  // the whole K loop: sleep instead of polling
     ptx::tc_fence_after();
-    const int x = x0 + warp * 32 + lane;
+    const int xl = warp * 32 + lane;  // pixel of the strip = TMEM lane
     const uint32_t tl = tmem + (uint32_t(warp * 32) << 16);
+    // The tile leaves through shared memory and TMA stores, 32 channels at a time: pixel xl's 64
+    // bytes go to staging row xl (or rows 2xl, 2xl+1 with the x2 upsample; the TMA box then covers
+    // 256 pixels and is stored to output rows 2y and 2y+1), in the 64-byte swizzle the map expects;
+    // out-of-range pixels / channels are clipped by the TMA.
 #pragma unroll 1
     for (int cb = 0; cb < kCoT; cb += 32) {
       uint32_t r[32];
       ptx::tmem_ld32(tl + cb, r);
       ptx::tmem_ld_wait();
-      if (x >= W) continue;
       float v[32];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int co = co0 + cb + i;
-        v[i] = u2f(r[i]) + (co < Co ? bias[co] : 0.f);
-        if (act_up) v[i] = v[i] / (1.f + expf(-v[i]));
+      for (int q = 0; q < 32; ++q) {
+        const int co = co0 + cb + q;
+        v[q] = u2f(r[q]) + (co < Co ? bias[co] : 0.f);
+        if (act_up) v[q] = v[q] / (1.f + expf(-v[q]));
       }
-      const int nco = min(32, Co - (co0 + cb));
-      if (nco <= 0) continue;
-      auto store = [&](int yy, int xx, int Wd) {
-        __nv_bfloat16* o = out + (int64_t(yy) * Wd + xx) * Co + co0 + cb;
-        if (nco == 32 && (Co % 8) == 0) {
+      uint4 pk[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            reinterpret_cast<uint4*>(o)[q] =
-                make_uint4(ptx::pack_bf16x2(v[8 * q], v[8 * q + 1]), ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
+      for (int q = 0; q < 4; ++q)
+        pk[q] = make_uint4(ptx::pack_bf16x2(v[8 * q], v[8 * q + 1]), ptx::pack_bf16x2(v[8 * q + 2], v[8 * q + 3]),
                            ptx::pack_bf16x2(v[8 * q + 4], v[8 * q + 5]), ptx::pack_bf16x2(v[8 * q + 6], v[8 * q + 7]));
-        } else {
+      if (cb > 0) {  // the previous chunk's TMA stores have read the staging buffer
+        if (threadIdx.x == 0) bulk_wait_read0();
+        ptx::named_bar_sync(1, 128);
+      }
+      const int nrow = act_up ? 2 : 1;
+      for (int rr = 0; rr < nrow; ++rr) {
+        const int row = act_up ? 2 * xl + rr : xl;
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (i < nco) o[i] = __float2bfloat16_rn(v[i]);
+        for (int q = 0; q < 4; ++q)
+          *reinterpret_cast<uint4*>(stage_out + row * 64 + ((q ^ ((row >> 1) & 3)) * 16)) = pk[q];
+      }
+      fence_proxy_async();
+      ptx::named_bar_sync(1, 128);
+      if (threadIdx.x == 0) {
+        if (act_up) {
+          tma_store_4d(&tmO, stage_out, co0 + cb, 2 * y, 2 * x0, 0);
+          tma_store_4d(&tmO, stage_out, co0 + cb, 2 * y + 1, 2 * x0, 0);
+        } else {
+          tma_store_4d(&tmO, stage_out, co0 + cb, y, x0, 0);
         }
-      };
-      if (act_up) {
-        store(2 * y, 2 * x, 2 * W);
-        store(2 * y, 2 * x + 1, 2 * W);
-        store(2 * y + 1, 2 * x, 2 * W);
-        store(2 * y + 1, 2 * x + 1, 2 * W);
-      } else {
-        store(y, x, W);
+        bulk_commit();
       }
     }
+    if (threadIdx.x == 0) bulk_wait0();
   }
   ptx::tc_fence_before();
   __syncthreads();
@@ -145,10 +169,15 @@ __global__ void __launch_bounds__(192, 2)
 cudaError_t launch_vae_conv_tc(const void* in, int Hout, int Ci, int W, const void* wt, const float* b, void* out,
                                int Co, int act_up, cudaStream_t st) {
   if (Hout == 0 || W == 0) return cudaSuccess;
-  CUtensorMap mx, mw;
+  CUtensorMap mx, mw, mo;
+  const int Co8 = (Co + 7) / 8 * 8;  // output channel stride (16-byte rows for the TMA store)
   // activations [Hout+2][W][Ci]: dims (Ci, rows->"H", pixels->"S"); box 64 channels x 128 pixels
   if (!make_map(&mx, in, 1, W, Hout + 2, Ci, int64_t(Hout + 2) * W * Ci, Ci, int64_t(W) * Ci, kKC, kPix) ||
-      !make_map(&mw, wt, 1, Co, 9, Ci, int64_t(9) * Co * Ci, Ci, int64_t(Co) * Ci, kKC, kCoT))
+      !make_map(&mw, wt, 1, Co, 9, Ci, int64_t(9) * Co * Ci, Ci, int64_t(Co) * Ci, kKC, kCoT) ||
+      // output [H'][W'][Co]: boxes of 32 channels (64B swizzle) x 128 (256 upsampled) pixels x 1 row
+      !make_map(&mo, out, 1, act_up ? 2 * W : W, act_up ? 2 * Hout : Hout, Co8,
+                int64_t(act_up ? 4 : 1) * Hout * W * Co8, Co8, int64_t(act_up ? 2 * W : W) * Co8, 32,
+                act_up ? 2 * kPix : kPix))
     return cudaErrorInvalidValue;
   static bool attr = false;
   if (!attr) {
@@ -157,7 +186,7 @@ cudaError_t launch_vae_conv_tc(const void* in, int Hout, int Ci, int W, const vo
     attr = true;
   }
   const dim3 grid((W + kPix - 1) / kPix, Hout, (Co + kCoT - 1) / kCoT);
-  vae_conv_tc_kernel<<<grid, 192, kSmem, st>>>(mx, mw, b, static_cast<__nv_bfloat16*>(out), Hout, W, Ci, Co, act_up);
+  vae_conv_tc_kernel<<<grid, 192, kSmem, st>>>(mx, mw, mo, b, Hout, W, Ci, Co, act_up);
   note_launches(1);
   return cudaGetLastError();
 }

@@ -69,13 +69,11 @@ def conv(ext, w, b, act_up: bool, stream=None):
     if ext.dtype == torch.bfloat16:
         Hp2, W, Ci = ext.shape
         H, Co = Hp2 - 2, w.shape[1]
-        out = torch.empty((2 * H, 2 * W, Co) if act_up else (H, W, Co), dtype=torch.bfloat16, device=ext.device)
+        # channels padded to a multiple of 8 (zeros): the kernel's TMA stores and the next conv's loads
+        out = torch.empty((2 * H, 2 * W, _pad8(Co)) if act_up else (H, W, _pad8(Co)), dtype=torch.bfloat16,
+                          device=ext.device)
         usp._check(usp.lib().xdit_vae_conv3x3_bf16(usp._ptr(ext), H, Ci, W, usp._ptr(w), usp._ptr(b), usp._ptr(out),
                                                    Co, 1 if act_up else 0, usp._stream(stream)), "xdit_vae_conv3x3_bf16")
-        if Co % 8 and act_up:  # the next conv needs Ci % 8 == 0 (TMA row stride): zero channels
-            pad = torch.zeros(out.shape[:2] + (_pad8(Co),), dtype=out.dtype, device=out.device)
-            pad[:, :, :Co] = out
-            out = pad
         return out
     Hp2, Ci, W = ext.shape
     H, Co = Hp2 - 2, w.shape[0]
