@@ -116,8 +116,10 @@ XDIT_API int xdit_comm_create(void* nccl_comm, int ulysses, int ring, xdit_comm_
  * (xdit_rowmap segment table).  Streams are ordered across ranks with
  * 32-bit flags in device memory (cuStreamWriteValue32 into the peer's flag after a system-wide
  * fence, cuStreamWaitValue32 >= on the local one): nothing spins on an SM and no host thread
- * waits, so xdit_usp_attention stays stream-ordered (but not graph-capturable: the flag values are
- * per-call epochs baked into the stream operations, so a capture is refused with UNSUPPORTED), and several ranks may
+ * waits, so xdit_usp_attention stays stream-ordered and CUDA-graph capturable (the flags are binary:
+ * the writer sets 1, the owner waits for 1 and resets 0 before the writer can set it again, so a
+ * captured call replays correctly; the mailbox and the peer cfg_tail use epochs and are not
+ * capturable), and several ranks may
  * share one GPU (one process per rank; ranks in one process are rejected).
  *
  * Setup, collective over the SP group (every rank, same order):
@@ -179,7 +181,7 @@ XDIT_API int xdit_p2p_wait_ack(xdit_comm_t comm, int receiver, uint32_t tag, xdi
 /* Allocates (or grows) the device workspace for a problem: Ulysses send/recv buffers, the
  * unpacked Q block, two ring KV slots, fp32 ring accumulators.  Call once per shape before the
  * hot loop (all ranks, same scalars); xdit_usp_attention never allocates, so the call path is
- * CUDA-graph capturable (N = 1 and the NCCL transport).  elem_bytes = 2 (bf16 path) or 4 (fp32 path).  S_txt/S_img are
+ * CUDA-graph capturable.  elem_bytes = 2 (bf16 path) or 4 (fp32 path).  S_txt/S_img are
  * GLOBAL token counts.  Errors: INVALID_ARG, DIVISIBILITY, EMPTY_SHARD, UNSUPPORTED, CUDA. */
 XDIT_API int xdit_comm_reserve(xdit_comm_t comm, int B, int H, int S_txt, int S_img, int D, int elem_bytes);
 

@@ -253,7 +253,6 @@ struct xdit_comm_s {
   int nranks = 1, rank = 0, u = 1, r = 1, device = 0;
   int transport = XDIT_TRANSPORT_NCCL;
   uint32_t* flags = nullptr;  // peer transport: kFlagWords words written by the peers
-  uint32_t epoch = 0;         // peer transport: calls issued (identical on every rank)
   bool connected = false;
   std::vector<PeerMap> peer;  // peer transport: per SP rank (self = local pointers)
   size_t mbox_region = 0;     // peer transport: mailbox bytes per source rank
@@ -280,6 +279,8 @@ int comm_finish_init(xdit_comm_s* c) {
     if (!memops()) return fail(XDIT_ERR_UNSUPPORTED, "stream memory operations (cuStreamWaitValue32) unavailable");
     XCUDA(cudaMalloc(&c->flags, kFlagWords * sizeof(uint32_t)));
     XCUDA(cudaMemset(c->flags, 0, kFlagWords * sizeof(uint32_t)));
+    const uint32_t one = 1;  // my ring successor's slot 1 is free before the first call
+    XCUDA(cudaMemcpy(c->flags + kFCredit + 1, &one, sizeof one, cudaMemcpyHostToDevice));
     XCUDA(cudaDeviceSynchronize());  // zeroed before any peer can map and write them
   } else if (c->nranks > 1) {
     const int i = c->rank / c->u, j = c->rank % c->u;
@@ -339,8 +340,6 @@ int wait_flag(cudaStream_t st, const uint32_t* flag, uint32_t v) {
   if (r != CUDA_SUCCESS) return fail(XDIT_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", int(r));
   return XDIT_OK;
 }
-// Ring step counter of the peer transport: epoch e, step s < 8.
-inline uint32_t ring_t(uint32_t e, int s) { return e * 8u + uint32_t(s); }
 
 // Byte-exact all-to-all of `chunk` bytes per peer on `comm` (send[p] -> peer p -> recv[p]).
 int a2a(ncclComm_t comm, int n, const void* send, void* recv, size_t chunk, cudaStream_t st) {
@@ -418,16 +417,9 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
                     need.kvslot);
     }
   }
-  if (peer) {
-    // the flag values are immediates of the stream memory operations: a captured call would replay
-    // the same epoch and its waits would pass on the previous replay's flags -- refuse capture
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    XCUDA(cudaStreamIsCapturing(st, &cs));
-    if (cs != cudaStreamCaptureStatusNone)
-      return fail(XDIT_ERR_UNSUPPORTED, "the peer transport cannot be captured in a CUDA graph (per-call epochs); "
-                  "use the NCCL transport or N = 1 for graphs");
-  }
-  const uint32_t e = peer ? ++c->epoch : 0u;  // every rank issues the same calls: epochs agree
+  // Peer transport flags are binary: the writer sets 1 (after its data), the owner waits for 1 and
+  // resets 0 before anything that lets the writer set it again -- so every stream operation carries
+  // constant values and the call replays correctly from a captured CUDA graph.
 
   const int i = P.i, Hh = P.Hh, L = P.S_loc[c->rank], Sb = P.S_blk[i];
   const int64_t row = int64_t(Hh) * D;  // elements per (token) row of a head-block tensor
@@ -469,9 +461,12 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
       for (int t = 0; t < 3; ++t)
         XCUDA(xdit::launch_uly_pack_to(src[t], pd, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
       for (int p = 0; p < P.u; ++p)
-        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFA2A + P.j, e));
+        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFA2A + P.j, 1));
       for (int p = 0; p < P.u; ++p)
-        if (p != P.j) XRET(wait_flag(st, c->flags + kFA2A + p, e));
+        if (p != P.j) {  // peer p sets it again only after my O return of this call (after this reset)
+          XRET(wait_flag(st, c->flags + kFA2A + p, 1));
+          XRET(post_flag(st, c->flags + kFA2A + p, 0));
+        }
     } else {
       for (int t = 0; t < 3; ++t)
         XCUDA(xdit::launch_uly_pack(src[t], c->uly_send.p, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
@@ -539,14 +534,18 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
   } else {
     // ---- a5-a7: ring loop; step s attends to the KV block of ring index (i - s) mod r (C9)
     const int nxt_peer = (i + 1) % P.r, prv_peer = (i - 1 + P.r) % P.r;
-    // peer transport: the ring neighbours' SP ranks, and slot-credit protocol.  Rank i pushes its
-    // current block into next's slot (s+1)&1 once next has posted that it finished reading that
-    // slot (credit = ring_t of its last read + 1): step s-1 of this call, or for s = 0 the last odd
-    // step of the previous call.  It posts its own credit for slot s&1 to prev after attention
-    // step s and after its own push out of that slot; next waits for data = ring_t(e, s) + 1.
+    // peer transport: slot credits.  Rank i pushes its current block into next's slot (s+1)&1 at
+    // step s <= r-2 once next's credit for that slot is set (it waits, resets, pushes, sets next's
+    // data flag).  A rank posts credit[s&1] to prev exactly once per push prev will make into that
+    // slot: after step 0 (slot 0, pushed at prev's step 1, if r >= 3), after steps 1..r-3 (pushed at
+    // prev's step s+1), and after its last odd step (slot 1, pushed at prev's step 0 of the NEXT
+    // call; credit[1] starts set).  Each post follows the reader's last use of the slot and its own
+    // push out of it, and every wait is matched by one post, so the flags end each call in the
+    // state they started it (credit[1] = 1, the rest 0).
     const PeerMap* pnext = peer ? &c->peer[nxt_peer * P.u + P.j] : nullptr;
     const PeerMap* pprev = peer ? &c->peer[prv_peer * P.u + P.j] : nullptr;
     const int last_odd = ((P.r - 1) & 1) ? P.r - 1 : P.r - 2;  // r >= 2
+    auto credit_after = [&](int st_) { return (st_ == 0 && P.r >= 3) || (st_ >= 1 && st_ <= P.r - 3) || st_ == last_odd; };
     const void* curK = Kc;
     const void* curV = Vc;
     xdit_rowmap accmap = plain_map(B, Sb, Hh, D);
@@ -561,11 +560,11 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
         const int nsrc = ((src - 1) % P.r + P.r) % P.r;
         const size_t sbytes = size_t(B) * Skv * row * eb, rbytes = size_t(B) * P.S_blk[nsrc] * row * eb;
         if (peer) {
-          const uint32_t credit = s >= 1 ? ring_t(e, s - 1) + 1 : (e > 1 ? ring_t(e - 1, last_odd) + 1 : 0u);
-          XRET(wait_flag(c->side, c->flags + kFCredit + nslot, credit));
+          XRET(wait_flag(c->side, c->flags + kFCredit + nslot, 1));
+          XRET(post_flag(c->side, c->flags + kFCredit + nslot, 0));
           XCUDA(cudaMemcpyAsync(pnext->ptr[kHKV + 2 * nslot], curK, sbytes, cudaMemcpyDefault, c->side));
           XCUDA(cudaMemcpyAsync(pnext->ptr[kHKV + 2 * nslot + 1], curV, sbytes, cudaMemcpyDefault, c->side));
-          XRET(post_flag(c->side, static_cast<uint32_t*>(pnext->ptr[kHFlags]) + kFData + nslot, ring_t(e, s) + 1));
+          XRET(post_flag(c->side, static_cast<uint32_t*>(pnext->ptr[kHFlags]) + kFData + nslot, 1));
           (void)rbytes;
         } else {
           XNCCL(ncclGroupStart());
@@ -597,8 +596,9 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
       if (s < P.r - 1) {
         XCUDA(cudaStreamWaitEvent(st, c->ev_recv[s & 1], 0));  // (peer: my push out of this block is done)
         if (peer) {
-          XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), ring_t(e, s) + 1));
-          XRET(wait_flag(st, c->flags + kFData + nslot, ring_t(e, s) + 1));
+          if (credit_after(s)) XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), 1));
+          XRET(wait_flag(st, c->flags + kFData + nslot, 1));
+          XRET(post_flag(st, c->flags + kFData + nslot, 0));
         }
         curK = c->kv[nslot][0].p;
         curV = c->kv[nslot][1].p;
@@ -607,8 +607,8 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
           XCUDA(xdit::launch_kv_retain(curK, curV, kv_keep, B, Hh, P.S_blk[nsrc], S_sp, blk_off(nsrc), D,
                                        int64_t(P.S_blk[nsrc]) * row, row, D, eb, st));
         }
-      } else if (peer) {  // last step: its slot's credit (read by prev's next call when s is odd)
-        XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), ring_t(e, s) + 1));
+      } else if (peer && credit_after(s)) {  // last step odd: slot 1's credit for prev's next call
+        XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), 1));
       }
     }
   }
@@ -617,9 +617,12 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
   if (P.u > 1) {
     if (peer) {  // the final epilogue already stored chunk p in peer p's receive buffer: flag, wait
       for (int p = 0; p < P.u; ++p)
-        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFO + P.j, e));
+        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFO + P.j, 1));
       for (int p = 0; p < P.u; ++p)
-        if (p != P.j) XRET(wait_flag(st, c->flags + kFO + p, e));
+        if (p != P.j) {  // peer p sets it again only after my next call's pack (after this reset)
+          XRET(wait_flag(st, c->flags + kFO + p, 1));
+          XRET(post_flag(st, c->flags + kFO + p, 0));
+        }
     } else {
       XCUDA(cudaEventRecord(c->ev_o, st));
       XCUDA(cudaStreamWaitEvent(c->side, c->ev_o, 0));
@@ -1044,6 +1047,10 @@ int xdit_cfg_tail(const void* eps_local, void* eps_gather, void* eps_out, int64_
     if (bytes > comm->mbox_region)
       return fail(XDIT_ERR_WORKSPACE, "cfg_tail: %zu bytes exceed the %zu-byte mailbox region "
                   "(xdit_comm_mailbox_reserve)", bytes, comm->mbox_region);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    XCUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs != cudaStreamCaptureStatusNone)  // its flags carry per-call epochs (immediates)
+      return fail(XDIT_ERR_UNSUPPORTED, "cfg_tail over the peer transport cannot be captured in a CUDA graph");
     const int me = comm->rank, other = 1 - me;
     const uint32_t e = ++comm->cfg_epoch;
     const PeerMap& m = comm->peer[other];

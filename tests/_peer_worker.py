@@ -224,8 +224,10 @@ def run_vae(rank: int, world: int, port: int, cases, out_dir: str):
         json.dump(res, f)
 
 
-def run_graph_refusal(rank: int, world: int, port: int, cases, out_dir: str):
-    """A peer-transport USP call inside CUDA-graph capture is refused (UNSUPPORTED), not mis-captured."""
+def run_graph(rank: int, world: int, port: int, cases, out_dir: str):
+    """The peer-transport USP call captured in a CUDA graph and replayed, interleaved with eager
+    calls: every replay equals the eager result bit for bit (binary set/reset flags carry constant
+    values, so the captured stream operations stay valid; include/xdit_usp.h)."""
     res = {"rank": rank, "checks": [], "error": None}
     try:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -238,27 +240,41 @@ def run_graph_refusal(rank: int, world: int, port: int, cases, out_dir: str):
 
         dist.init_process_group("gloo", rank=rank, world_size=world)
         torch.cuda.set_device(0)
-        comm = usp.Comm(world, 1, transport="peer")
-        q, k, v = (t[:, rank * 64:(rank + 1) * 64].contiguous().cuda() for t in qkv(1, 64 * world, 2 * world, 64, seed=1))
-        usp.attention(q, k, v, S_txt=0, S_img=64 * world, comm=comm, ulysses=world, ring=1)  # reserve + eager call
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        s = torch.cuda.Stream()
-        refused = False
-        with torch.cuda.stream(s):
-            try:
+        for (u, r) in cases:
+            comm = usp.Comm(u, r, transport="peer")
+            S_txt, S_img, H, D = 7, 300, 8, 64
+            q, k, v = qkv(1, S_txt + S_img, H, D, seed=11 + u)
+            to, tl, io, il = usp.shard(S_txt, S_img, world, rank)
+            idx = torch.cat([torch.arange(to, to + tl), S_txt + torch.arange(io, io + il)])
+            ql, kl, vl = (t[:, idx].contiguous().cuda() for t in (q, k, v))
+            kw = dict(S_txt=S_txt, S_img=S_img, comm=comm, ulysses=u, ring=r)
+            ref_o, ref_l = usp.attention(ql, kl, vl, **kw)  # eager (reserve + connect happen here)
+            torch.cuda.synchronize()
+            out = torch.empty_like(ref_o)
+            lse = torch.empty_like(ref_l)
+            g = torch.cuda.CUDAGraph()
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(s):
                 with torch.cuda.graph(g, stream=s):
-                    usp.attention(q, k, v, S_txt=0, S_img=64 * world, comm=comm, ulysses=world, ring=1)
-            except usp.XditError as e:
-                refused = e.status == "UNSUPPORTED"
-            except RuntimeError:
-                pass  # capture aborted by the raise inside it
-        assert refused, "capture of a peer-transport call was not refused"
-        res["checks"].append({"refused": True})
-        torch.cuda.synchronize()
-        dist.barrier()
-        comm.destroy()
-        dist.barrier()
+                    usp.attention(ql, kl, vl, out=out, lse=lse, **kw)
+            torch.cuda.synchronize()
+            for rep in range(4):
+                out.zero_()
+                lse.zero_()
+                g.replay()
+                if rep == 1:  # an eager call between replays keeps the flag states in step
+                    o2, l2 = usp.attention(ql, kl, vl, **kw)
+                    torch.cuda.synchronize()
+                    assert torch.equal(o2, ref_o) and torch.equal(l2, ref_l), "eager call after a replay differs"
+                torch.cuda.synchronize()
+                assert torch.equal(out, ref_o) and torch.equal(lse, ref_l), f"replay {rep} differs (u={u}, r={r})"
+            res["checks"].append({"u": u, "r": r})
+            torch.cuda.synchronize()
+            dist.barrier()
+            del g
+            comm.destroy()
+            dist.barrier()
         dist.destroy_process_group()
     except Exception:
         res["error"] = traceback.format_exc()

@@ -105,11 +105,12 @@ def test_vae_band_processes(world):
     assert all(len(r["checks"]) == len(cases) for r in out)
 
 
-def test_peer_transport_refuses_graph_capture():
-    """The peer transport bakes per-call epochs into its stream operations, so a captured call could
-    not be replayed safely: capture is refused with XDIT_ERR_UNSUPPORTED (include/xdit_usp.h)."""
-    out = _run_world(2, None, None, fn="run_graph_refusal")
-    assert all(r["checks"] for r in out)
+@pytest.mark.parametrize("world,splits", [(2, [(2, 1), (1, 2)]), (4, [(2, 2), (1, 4)])])
+def test_peer_transport_graph_replay(world, splits):
+    """The peer-transport USP call captured in a CUDA graph replays bit-identically (4 replays with
+    an eager call in between) for Ulysses, Ring and hybrid splits."""
+    out = _run_world(world, None, splits, fn="run_graph")
+    assert all(len(r["checks"]) == len(splits) for r in out)
 
 
 def test_peer_transport_error_paths():
