@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
                     help="multi-rank byte movement: the library's peer-memory transport or NCCL")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="N > 1: time eager calls instead of replaying the step captured in a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
     return ap.parse_args()
 
@@ -296,6 +298,29 @@ def main():
     for _ in range(args.warmup):
         step()
     barrier()
+    # N > 1: the step (a dozen kernels and stream flag operations per call) is captured once in a
+    # CUDA graph and replayed -- the peer transport's binary flags make replays valid -- so host
+    # enqueue cost does not pace the short multi-rank calls.  Falls back to eager calls if capture fails.
+    graph, graph_note = None, None
+    n_pre = usp.launch_count()
+    if N > 1 and not args.no_graph:
+        try:
+            cs = torch.cuda.Stream(device=dev)
+            cs.wait_stream(stream)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g, stream=cs):
+                    step()
+            torch.cuda.synchronize()
+            g.replay()  # one untimed replay
+            barrier()
+            graph = g
+        except Exception as ex:  # noqa: BLE001 -- reported in the JSON line
+            graph_note = f"capture failed, eager: {type(ex).__name__}: {ex}"[:200]
+            torch.cuda.synchronize()
+            barrier()
+    n_captured = usp.launch_count()
+    timed_step = graph.replay if graph is not None else step
     n0 = usp.launch_count()
     with ClockSampler(local) as clocks:
         if not flush:
@@ -303,7 +328,7 @@ def main():
             barrier()
             e0.record(stream)
             for _ in range(args.steps):
-                step()
+                timed_step()
             e1.record(stream)
             barrier()
             ms = e0.elapsed_time(e1) / args.steps
@@ -314,12 +339,15 @@ def main():
                 barrier()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                step()
+                timed_step()
                 e1.record(stream)
                 barrier()
                 tot += e0.elapsed_time(e1)
             ms = tot / args.steps
     launches = (usp.launch_count() - n0) // args.steps
+    if graph is not None:  # replays launch the captured kernels without passing through the library:
+        launches = n_captured - n_pre  # the library's launches recorded into the graph (one call)
+
     ms = max_over_ranks(ms)
     flops = w.flops()  # whole job (all CFG groups)
     tflops = flops / (ms * 1e-3) / 1e12
@@ -449,6 +477,8 @@ def main():
             "config": {"workload": w.name, "B": w.B * w.cfg, "H": w.H, "D": w.D, "S_txt": w.S_txt,
                        "S_img": w.S_img, "cfg": cfg, "ulysses": u, "ring": r,
                        "transport": comm.transport if sp > 1 else None,
+                       "cuda_graph": graph is not None,
+                       **({"cuda_graph_note": graph_note} if graph_note else {}),
                        **({"shared_gpu": True} if share and N > 1 else {}),
                        "l2": "flushed between steps" if flush else "inputs larger than L2"},
             "ms_per_layer": ms,
