@@ -28,6 +28,15 @@ struct EpiParams {
   // by tail_merge_kernel -- this fills the last, partial wave of the grid.
   int n_qt, n_full, n_split, kv_chunk;
   float* part;  // [n_tail * n_split][256][D] fp32 O, then [n_tail * n_split][256] fp32 LSE
+  // Ring merge fused into the epilogue (a7, reading C9; CTA-pair kernel): merge = 1 combines this
+  // launch's (O_s, LSE_s) row with the accumulator row (acc_o, acc_l_in; layout acc_map) by their
+  // log-sum-exp; merge_final = 0 writes the result back to acc_o (in place) and acc_l_out, 1 writes
+  // it to the final destination (o, lse through map, bf16 or fp32).
+  int merge, merge_final;
+  float* acc_o;
+  const float* acc_l_in;
+  float* acc_l_out;
+  xdit_rowmap acc_map;
   int diag;  // profiling only (XDIT_DIAG): 1 = softmax does no math, 2 = also no MMA<-softmax wait
   unsigned long long* trace;  // profiling only (XDIT_TRACE): per-iteration clock64 stamps of CTA 0
 };
@@ -105,15 +114,36 @@ __global__ void __launch_bounds__(256)
   for (int s = 0; s < n_split; ++s) M = fmaxf(M, plse[(int64_t(ti) * n_split + s) * kRowsPerItem + rr]);
   float sum = 0.f;
   for (int s = 0; s < n_split; ++s) sum += expf(plse[(int64_t(ti) * n_split + s) * kRowsPerItem + rr] - M);
-  const float L = M + logf(sum);
+  const float Ls = M + logf(sum);  // LSE of this launch's key range
+  float L = Ls;
   const RowDst dst = rowmap_dst(p.map, b, row, h);
+  // fused ring merge (p.merge): combine with the accumulator row, as lse_merge_kernel does
+  float wa = 0.f, wb = 1.f;
+  RowDst ad{0, 0};
+  if (p.merge) {
+    ad = rowmap_dst(p.acc_map, b, row, h);
+    const float la = p.acc_l_in[ad.l_off];
+    const float M2 = fmaxf(la, L);
+    const float L2 = M2 + logf(expf(la - M2) + expf(L - M2));
+    wa = expf(la - L2);
+    wb = expf(L - L2);
+    L = L2;
+  }
   for (int d = lane * 4; d < D; d += 128) {
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < n_split; ++s) {
       const int64_t pr = (int64_t(ti) * n_split + s) * kRowsPerItem + rr;
-      const float wgt = expf(plse[pr] - L);
+      const float wgt = expf(plse[pr] - Ls);
       const float4 x = *reinterpret_cast<const float4*>(part + pr * D + d);
       acc.x += wgt * x.x; acc.y += wgt * x.y; acc.z += wgt * x.z; acc.w += wgt * x.w;
+    }
+    if (p.merge) {
+      const float4 y = *reinterpret_cast<const float4*>(p.acc_o + ad.o_off + d);
+      acc = make_float4(wa * y.x + wb * acc.x, wa * y.y + wb * acc.y, wa * y.z + wb * acc.z, wa * y.w + wb * acc.w);
+      if (!p.merge_final) {
+        *reinterpret_cast<float4*>(p.acc_o + ad.o_off + d) = acc;
+        continue;
+      }
     }
     if (p.out_f32) {
       *reinterpret_cast<float4*>(static_cast<float*>(p.o) + dst.o_off + d) = acc;
@@ -124,7 +154,10 @@ __global__ void __launch_bounds__(256)
       *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(p.o) + dst.o_off + d) = v;
     }
   }
-  if (lane == 0 && p.lse) p.lse[dst.l_off] = L;
+  if (lane == 0) {
+    if (p.merge && !p.merge_final) p.acc_l_out[ad.l_off] = L;
+    else if (p.lse) p.lse[dst.l_off] = L;
+  }
 }
 
 // ------------------------------------------------------------------ host side

@@ -471,6 +471,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     void* obase = p.o;
     float* lbase = p.lse;
     int of32 = p.out_f32;
+    float lse_row = (m_used + log2f(l)) * 0.69314718055994530942f;
+    // fused ring merge (a7): O = wa * O_acc + wb * O_s, LSE by log-sum-exp (lse_merge_kernel's
+    // arithmetic); wb folds in 1/l.  Results go back to the accumulator or, at the last ring step,
+    // to the final destination.
+    const bool mrg = p.merge && piece < 0 && row < p.Sq;
+    float wa = 0.f, wbl = inv_l;
+    RowDst ad{0, 0};
+    if (mrg) {
+      ad = rowmap_dst(p.acc_map, b, row, h);
+      const float la = p.acc_l_in[ad.l_off];
+      const float M2 = fmaxf(la, lse_row);
+      const float L2 = M2 + logf(expf(la - M2) + expf(lse_row - M2));
+      wa = expf(la - L2);
+      wbl = expf(lse_row - L2) * inv_l;
+      lse_row = L2;
+      if (!p.merge_final) {
+        obase = p.acc_o;
+        lbase = p.acc_l_out;
+        of32 = 1;
+        dst = ad;
+      }
+    }
     if (piece >= 0) {  // split tail item: normalised fp32 partial for tail_merge_kernel
       const int64_t prow = int64_t(piece) * kRowsPerItem + int(rank) * kRows + row_in_tile;
       const int64_t n_pieces = int64_t(gridDim.x >> 1) - p.n_full;
@@ -486,21 +508,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t o[32];
       ptx::tmem_ld32(tO + col, o);
       ptx::tmem_ld_wait();
+      if (mrg) {  // o <- wa * acc + wb * O_s, then stored with inv_l = 1
+        const float4* ap = reinterpret_cast<const float4*>(p.acc_o + ad.o_off + col);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 y = ap[i];
+          o[4 * i] = f2u(fmaf(wbl, u2f(o[4 * i]), wa * y.x));
+          o[4 * i + 1] = f2u(fmaf(wbl, u2f(o[4 * i + 1]), wa * y.y));
+          o[4 * i + 2] = f2u(fmaf(wbl, u2f(o[4 * i + 2]), wa * y.z));
+          o[4 * i + 3] = f2u(fmaf(wbl, u2f(o[4 * i + 3]), wa * y.w));
+        }
+      }
+      const float sc = mrg ? 1.f : inv_l;
       if (valid_row) {
         if (of32) {
           float4* dp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + col);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
-            dp[i] = make_float4(u2f(o[4 * i]) * inv_l, u2f(o[4 * i + 1]) * inv_l, u2f(o[4 * i + 2]) * inv_l,
-                                u2f(o[4 * i + 3]) * inv_l);
+            dp[i] = make_float4(u2f(o[4 * i]) * sc, u2f(o[4 * i + 1]) * sc, u2f(o[4 * i + 2]) * sc,
+                                u2f(o[4 * i + 3]) * sc);
         } else {
           uint4* dp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + col);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
-            dp[i] = make_uint4(ptx::pack_bf16x2(u2f(o[8 * i]) * inv_l, u2f(o[8 * i + 1]) * inv_l),
-                               ptx::pack_bf16x2(u2f(o[8 * i + 2]) * inv_l, u2f(o[8 * i + 3]) * inv_l),
-                               ptx::pack_bf16x2(u2f(o[8 * i + 4]) * inv_l, u2f(o[8 * i + 5]) * inv_l),
-                               ptx::pack_bf16x2(u2f(o[8 * i + 6]) * inv_l, u2f(o[8 * i + 7]) * inv_l));
+            dp[i] = make_uint4(ptx::pack_bf16x2(u2f(o[8 * i]) * sc, u2f(o[8 * i + 1]) * sc),
+                               ptx::pack_bf16x2(u2f(o[8 * i + 2]) * sc, u2f(o[8 * i + 3]) * sc),
+                               ptx::pack_bf16x2(u2f(o[8 * i + 4]) * sc, u2f(o[8 * i + 5]) * sc),
+                               ptx::pack_bf16x2(u2f(o[8 * i + 6]) * sc, u2f(o[8 * i + 7]) * sc));
         }
       }
     }
@@ -509,21 +543,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t o[8];
       ptx::tmem_ld8(tO + col, o);
       ptx::tmem_ld_wait();
+      if (mrg) {
+        const float4* ap = reinterpret_cast<const float4*>(p.acc_o + ad.o_off + col);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+          const float4 y = ap[i];
+          o[4 * i] = f2u(fmaf(wbl, u2f(o[4 * i]), wa * y.x));
+          o[4 * i + 1] = f2u(fmaf(wbl, u2f(o[4 * i + 1]), wa * y.y));
+          o[4 * i + 2] = f2u(fmaf(wbl, u2f(o[4 * i + 2]), wa * y.z));
+          o[4 * i + 3] = f2u(fmaf(wbl, u2f(o[4 * i + 3]), wa * y.w));
+        }
+      }
+      const float sc = mrg ? 1.f : inv_l;
       if (valid_row) {
         if (of32) {
           float4* dp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + col);
-          dp[0] = make_float4(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l, u2f(o[2]) * inv_l, u2f(o[3]) * inv_l);
-          dp[1] = make_float4(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l, u2f(o[6]) * inv_l, u2f(o[7]) * inv_l);
+          dp[0] = make_float4(u2f(o[0]) * sc, u2f(o[1]) * sc, u2f(o[2]) * sc, u2f(o[3]) * sc);
+          dp[1] = make_float4(u2f(o[4]) * sc, u2f(o[5]) * sc, u2f(o[6]) * sc, u2f(o[7]) * sc);
         } else {
           uint4* dp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + col);
-          dp[0] = make_uint4(ptx::pack_bf16x2(u2f(o[0]) * inv_l, u2f(o[1]) * inv_l),
-                             ptx::pack_bf16x2(u2f(o[2]) * inv_l, u2f(o[3]) * inv_l),
-                             ptx::pack_bf16x2(u2f(o[4]) * inv_l, u2f(o[5]) * inv_l),
-                             ptx::pack_bf16x2(u2f(o[6]) * inv_l, u2f(o[7]) * inv_l));
+          dp[0] = make_uint4(ptx::pack_bf16x2(u2f(o[0]) * sc, u2f(o[1]) * sc),
+                             ptx::pack_bf16x2(u2f(o[2]) * sc, u2f(o[3]) * sc),
+                             ptx::pack_bf16x2(u2f(o[4]) * sc, u2f(o[5]) * sc),
+                             ptx::pack_bf16x2(u2f(o[6]) * sc, u2f(o[7]) * sc));
         }
       }
     }
-    if (c == 0 && valid_row && lbase) lbase[dst.l_off] = (m_used + log2f(l)) * 0.69314718055994530942f;
+    if (c == 0 && valid_row && lbase) lbase[dst.l_off] = piece >= 0 ? (m_used + log2f(l)) * 0.69314718055994530942f
+                                                                 : lse_row;
   }
   __syncwarp();
   ptx::tc_fence_before();
@@ -572,6 +619,12 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.Sq = a.Sq;
   p.Skv = a.Skv;
   p.out_f32 = a.out_f32;
+  p.merge = a.merge;
+  p.merge_final = a.merge_final;
+  p.acc_o = a.acc_o;
+  p.acc_l_in = a.acc_l_in;
+  p.acc_l_out = a.acc_l_out;
+  p.acc_map = a.acc_map;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
   static const int diag = [] {
     const char* e = std::getenv("XDIT_DIAG");

@@ -788,13 +788,21 @@ size_t attn_scratch_floats(int D) {
   return size_t(nsm) * (kQTiles * kBlockM) * size_t(D + 1);
 }
 
-cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st) {
-  if (a.Sq == 0 || a.B == 0) return cudaSuccess;
+static bool force_1sm_kernel() {
   // XDIT_ATTN_KERNEL=1sm forces the one-CTA kernel where the CTA-pair kernel would run.
-  static const bool force_1sm = [] {
+  static const bool force = [] {
     const char* e = std::getenv("XDIT_ATTN_KERNEL");
     return e && std::string(e) == "1sm";
   }();
+  return force;
+}
+
+bool attn_fused_merge_supported(int D) { return !force_1sm_kernel() && attn_fwd_2sm_supports(D); }
+
+cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st) {
+  if (a.Sq == 0 || a.B == 0) return cudaSuccess;
+  const bool force_1sm = force_1sm_kernel();
+  if (a.merge && (force_1sm || !attn_fwd_2sm_supports(a.D))) return cudaErrorInvalidValue;
   if (!force_1sm && attn_fwd_2sm_supports(a.D)) return launch_attn_fwd_2sm(a, st);
   switch (a.D) {
     case 64: return launch_d<64>(a, st);

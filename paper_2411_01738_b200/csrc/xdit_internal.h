@@ -26,7 +26,16 @@ struct AttnArgs {
   int out_f32;
   float* scratch = nullptr;    // optional fp32 scratch for the tail split (bf16 kernel), may be null
   size_t scratch_floats = 0;
+  // ring merge fused into the epilogue (see EpiParams in attn_common.cuh); only where
+  // attn_fused_merge_supported() says so
+  int merge = 0, merge_final = 0;
+  float* acc_o = nullptr;
+  const float* acc_l_in = nullptr;
+  float* acc_l_out = nullptr;
+  xdit_rowmap acc_map{};
 };
+// True when launch_attn_fwd_sm100 would run a kernel that implements the fused ring merge.
+bool attn_fused_merge_supported(int D);
 
 // fp32 scratch the bf16 attention kernel can use to split the last partial wave of its grid:
 // (#SMs) x 256 rows x (D + 1) floats.

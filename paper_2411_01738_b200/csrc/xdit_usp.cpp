@@ -549,6 +549,12 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     const void* curK = Kc;
     const void* curV = Vc;
     xdit_rowmap accmap = plain_map(B, Sb, Hh, D);
+    // a7 fused into the attention epilogue where the kernel supports it (bf16 CTA-pair kernel): step
+    // s >= 1 merges its rows into O_acc in place (LSE_acc double-buffered: lacc <-> ltmp), the last
+    // step writes the merged result straight to its final destination -- no fp32 partial round trip
+    const bool fuse = dtype == 0 && xdit::attn_fused_merge_supported(D);
+    float* l_in = static_cast<float*>(c->lacc.p);
+    float* l_out = static_cast<float*>(c->ltmp.p);
     for (int s = 0; s < P.r; ++s) {
       const int src = ((i - s) % P.r + P.r) % P.r;
       const int Skv = P.S_blk[src];
@@ -579,13 +585,26 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
       a.k = curK; a.v = curV; a.Skv = Skv;
       a.kv_b = int64_t(Skv) * row; a.kv_s = row; a.kv_h = D;
       a.omap = accmap; a.out_f32 = 1;
+      a.merge = 0;
       if (s == 0) {
         a.o = c->oacc.p; a.lse = static_cast<float*>(c->lacc.p);
+      } else if (fuse) {
+        const bool last = s == P.r - 1;
+        a.merge = 1;
+        a.merge_final = last ? 1 : 0;
+        a.acc_o = static_cast<float*>(c->oacc.p);
+        a.acc_l_in = l_in;
+        a.acc_l_out = l_out;
+        a.acc_map = accmap;
+        if (last) {
+          a.o = dst; a.lse = dst_lse; a.omap = fmap; a.out_f32 = dtype;
+        }
       } else {
         a.o = c->otmp.p; a.lse = static_cast<float*>(c->ltmp.p);
       }
       XRET(attn_launch(a, dtype, st, &c->tail));
-      if (s > 0) {
+      if (fuse && s > 0) std::swap(l_in, l_out);
+      if (s > 0 && !fuse) {
         const bool last = s == P.r - 1;
         XCUDA(xdit::launch_lse_merge(static_cast<float*>(c->oacc.p), static_cast<float*>(c->lacc.p),
                                      static_cast<const float*>(c->otmp.p),

@@ -116,3 +116,12 @@ def test_peer_transport_graph_replay(world, splits):
 def test_peer_transport_error_paths():
     out = _run_world(2, None, None, fn="run_errors")
     assert all(r["checks"] == ["not_connected", "workspace", "mismatch"] for r in out)
+
+
+@pytest.mark.parametrize("world,splits", [(2, [(1, 2)]), (4, [(1, 4), (2, 2)])])
+def test_peer_ring_fused_merge_with_tail_split(world, splits):
+    """Ring splits on a ring block large enough that the attention grid's last partial wave is split
+    over key ranges (tail_merge_kernel), so the ring merge fused into the epilogue AND into the tail
+    merge both run (a7), against the fp64 oracle; D = 64 and 128."""
+    cases = [(2, 8, 40, 2600 * world // 2, 64, "bf16", False), (1, 8, 17, 5200 * world // 2, 128, "bf16", False)]
+    _run_world(world, splits, cases)
