@@ -19,16 +19,24 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "attn_common.cuh"
 
 namespace xdit {
 namespace {
 
-constexpr int kPix = 128, kCoT = 128, kKC = 64, kStages = 3;  // 3 stages: 2 CTAs per SM (one's epilogue overlaps the other's K loop)
-constexpr int kTileA = kPix * kKC * 2, kTileB = kCoT * kKC * 2;  // 16 KB each
-constexpr int kStageBytes = kTileA + kTileB;
-constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+constexpr int kPix = 128, kKC = 64;
+constexpr int kTileA = kPix * kKC * 2;  // 16 KB
+// Output-channel block COT = 128 (3 stages) or 256 (2 stages, half the A-tile loads per FLOP, one
+// N = 256 MMA per K step): either way 2 CTAs per SM, so one CTA's epilogue overlaps the other's K loop.
+template <int COT>
+struct TC {
+  static constexpr int kCoT = COT, kStages = COT == 256 ? 2 : 3;
+  static constexpr int kTileB = COT * kKC * 2;
+  static constexpr int kStageBytes = kTileA + kTileB;
+  static constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+};
 
 // TMA store of a 4-D box from shared memory (bulk-group completion) and its helpers.
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2,
@@ -43,10 +51,13 @@ __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
+template <int COT>
 __global__ void __launch_bounds__(192, 2)
     vae_conv_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW,
                        const __grid_constant__ CUtensorMap tmO, const float* __restrict__ bias, int Hout, int W,
                        int Ci, int Co, int act_up) {
+  using T = TC<COT>;
+  constexpr int kCoT = T::kCoT, kStages = T::kStages, kStageBytes = T::kStageBytes;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   // output staging (up to 256 pixels x 32 channels bf16 = 16 KB, 64B swizzle atoms): the operand
@@ -68,7 +79,7 @@ __global__ void __launch_bounds__(192, 2)
     ptx::fence_mbar_init();
   }
   if (warp == 5) {
-    ptx::tmem_alloc(tmem_slot, 128);
+    ptx::tmem_alloc(tmem_slot, kCoT);
     ptx::tmem_relinquish();
   }
   ptx::tc_fence_before();
@@ -161,34 +172,51 @@ __global__ void __launch_bounds__(192, 2)
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 5) ptx::tmem_dealloc(tmem, 128);
+  if (warp == 5) ptx::tmem_dealloc(tmem, kCoT);
 }
 
+}  // namespace
+
+namespace {
+template <int COT>
+cudaError_t launch_tc(const CUtensorMap& mx, const void* wt, const CUtensorMap& mo, const float* b, int Hout, int Ci,
+                      int W, int Co, int act_up, cudaStream_t st) {
+  using T = TC<COT>;
+  CUtensorMap mw;
+  if (!make_map(&mw, wt, 1, Co, 9, Ci, int64_t(9) * Co * Ci, Ci, int64_t(Co) * Ci, kKC, COT))
+    return cudaErrorInvalidValue;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(vae_conv_tc_kernel<COT>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const dim3 grid((W + kPix - 1) / kPix, Hout, (Co + COT - 1) / COT);
+  vae_conv_tc_kernel<COT><<<grid, 192, T::kSmem, st>>>(mx, mw, mo, b, Hout, W, Ci, Co, act_up);
+  note_launches(1);
+  return cudaGetLastError();
+}
 }  // namespace
 
 cudaError_t launch_vae_conv_tc(const void* in, int Hout, int Ci, int W, const void* wt, const float* b, void* out,
                                int Co, int act_up, cudaStream_t st) {
   if (Hout == 0 || W == 0) return cudaSuccess;
-  CUtensorMap mx, mw, mo;
+  CUtensorMap mx, mo;
   const int Co8 = (Co + 7) / 8 * 8;  // output channel stride (16-byte rows for the TMA store)
   // activations [Hout+2][W][Ci]: dims (Ci, rows->"H", pixels->"S"); box 64 channels x 128 pixels
   if (!make_map(&mx, in, 1, W, Hout + 2, Ci, int64_t(Hout + 2) * W * Ci, Ci, int64_t(W) * Ci, kKC, kPix) ||
-      !make_map(&mw, wt, 1, Co, 9, Ci, int64_t(9) * Co * Ci, Ci, int64_t(Co) * Ci, kKC, kCoT) ||
-      // output [H'][W'][Co]: boxes of 32 channels (64B swizzle) x 128 (256 upsampled) pixels x 1 row
+      // output [H'][W'][Co8]: boxes of 32 channels (64B swizzle) x 128 (256 upsampled) pixels x 1 row
       !make_map(&mo, out, 1, act_up ? 2 * W : W, act_up ? 2 * Hout : Hout, Co8,
                 int64_t(act_up ? 4 : 1) * Hout * W * Co8, Co8, int64_t(act_up ? 2 * W : W) * Co8, 32,
                 act_up ? 2 * kPix : kPix))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(vae_conv_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const dim3 grid((W + kPix - 1) / kPix, Hout, (Co + kCoT - 1) / kCoT);
-  vae_conv_tc_kernel<<<grid, 192, kSmem, st>>>(mx, mw, mo, b, Hout, W, Ci, Co, act_up);
-  note_launches(1);
-  return cudaGetLastError();
+  static const int cot = [] {  // XDIT_VAE_COT=128|256 overrides the choice (A/B)
+    const char* e = std::getenv("XDIT_VAE_COT");
+    return e ? std::atoi(e) : 0;
+  }();
+  const bool wide = cot ? cot == 256 : Co >= 256;
+  return wide ? launch_tc<256>(mx, wt, mo, b, Hout, Ci, W, Co, act_up, st)
+              : launch_tc<128>(mx, wt, mo, b, Hout, Ci, W, Co, act_up, st);
 }
 
 }  // namespace xdit
