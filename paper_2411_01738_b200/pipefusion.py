@@ -160,7 +160,7 @@ def run_stage(x0, weights, comm, *, T: int, M: int, warmup: int, sigma: float, S
     # covers them all), so a sender only waits for the receiver to have consumed the message of step
     # s - 2 in that space -- never one of the current step, which would close a cycle with stage 0
     # consuming the eps of step s only while it runs step s + 1.
-    tags = comm.__dict__.setdefault("_pf_tags", {"in": 0, "out": 0, "last": {}})
+    tags = comm.p2p_tags.setdefault("pipefusion", {"in": 0, "out": 0, "last": {}})
     tag_in, tag_out, last = tags["in"], tags["out"], tags["last"]
     row_bytes = H * D * eb
     if tag_out:  # a new call (shapes may differ): everything sent before has been consumed

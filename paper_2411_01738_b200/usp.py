@@ -210,6 +210,9 @@ class Comm:
             self.rank = rank
         self.handle = h
         self._reserved = None
+        # per-channel message counters of mailbox users (PipeFusion stages, VAE bands): the device
+        # flags keep their values across calls, so the tags must continue where the last call ended
+        self.p2p_tags = {}
 
     def reserve(self, B: int, H: int, S_txt: int, S_img: int, D: int, elem_bytes: int = 2):
         """Collective when the shape changes (every rank, same scalars): reserve the workspace and,

@@ -113,7 +113,7 @@ def decode_band(band, dec: Decoder, comm):
         W = 2 * W if i < len(dec.layers) - 1 else W
     rb = (max(rows) + 255) // 256 * 256
     comm.mailbox(2 * rb)
-    tags = comm.__dict__.setdefault("_vae_tags", {})
+    tags = comm.p2p_tags.setdefault("vae", {})
     x = band
     for i, (w, b) in enumerate(dec.layers):
         h = x.shape[0]
