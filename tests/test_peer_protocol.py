@@ -1,4 +1,5 @@
-"""Model check of the peer transport's ring flag protocol (xdit_usp.cpp usp_call).
+"""Model check of the peer transport's flag protocols (xdit_usp.cpp usp_call):
+the ring K/V rotation and the Ulysses exchange.
 
 The GPU tests run the real protocol with 2-8 processes; this CPU test explores it exhaustively-ish
 under random interleavings of every rank's two streams, on a model that enqueues exactly the
@@ -57,12 +58,10 @@ def simulate(r, calls, seed):
     flags = [{("data", 0): 0, ("data", 1): 0, ("credit", 0): 0, ("credit", 1): 1} for _ in range(r)]
     # slot contents: (call, ring index of the block); "local" block is separate
     slot = [[None, None] for _ in range(r)]
-    reading = [[0, 0] for _ in range(r)]  # owner's reads in flight per slot (reads are atomic here)
     marks = [set() for _ in range(r)]
     evs = [set() for _ in range(r)]
     progs = [build_program(i, r, calls) for i in range(r)]
     pc = [[0, 0] for _ in range(r)]
-    last_read = [[None, None] for _ in range(r)]  # (call, step) of the owner's last read per slot
     pending_read = [[[] for _ in range(2)] for _ in range(r)]  # blocks the owner still has to read
 
     def cur_block(i, c, s):
@@ -143,3 +142,78 @@ def test_credit_posts_match_pushes():
         for s in range(r - 1):
             pushes[(s + 1) & 1] += 1
         assert posts == pushes, (r, posts, pushes)
+
+
+def simulate_ulysses(u, calls, seed):
+    """Model of the Ulysses exchange (one stream per rank): pack = stores into every peer's receive
+    chunk [me], set A2A[me] on each peer, wait + reset my A2A[p] for all p != me, unpack (reads my
+    receive buffer), epilogue = stores into every peer's O chunk [me], set O[me] on each peer, wait +
+    reset my O[p], unpack_out (reads my O buffer)."""
+    rng = random.Random(seed)
+    flags = [{(k, p): 0 for k in ("a2a", "o") for p in range(u)} for _ in range(u)]
+    recv = [[None] * u for _ in range(u)]   # recv[owner][writer] = call of the chunk
+    orecv = [[None] * u for _ in range(u)]
+    unread = [[False] * u for _ in range(u)]
+    ounread = [[False] * u for _ in range(u)]
+    prog = []
+    for i in range(u):
+        ops = []
+        for c in range(calls):
+            ops.append(("pack", c))
+            ops += [("set", ("a2a", p)) for p in range(u) if p != i]
+            for p in range(u):
+                if p != i:
+                    ops += [("wait", ("a2a", p)), ("reset", ("a2a", p))]
+            ops.append(("unpack", c))
+            ops.append(("epilogue", c))
+            ops += [("set", ("o", p)) for p in range(u) if p != i]
+            for p in range(u):
+                if p != i:
+                    ops += [("wait", ("o", p)), ("reset", ("o", p))]
+            ops.append(("unpack_out", c))
+        prog.append(ops)
+    pc = [0] * u
+
+    def step(i):
+        if pc[i] >= len(prog[i]):
+            return False
+        kind, a = prog[i][pc[i]]
+        if kind == "pack":
+            for p in range(u):
+                assert not unread[p][i], f"rank {i} overwrote {p}'s receive chunk before it was unpacked"
+                recv[p][i], unread[p][i] = a, True
+        elif kind == "set":
+            k, p = a
+            assert flags[p][(k, i)] == 0, "lost signal"
+            flags[p][(k, i)] = 1
+        elif kind == "wait":
+            if flags[i][a] < 1:
+                return False
+        elif kind == "reset":
+            flags[i][a] = 0
+        elif kind == "unpack":
+            assert all(recv[i][p] == a for p in range(u)), "unpacked a chunk of another call"
+            unread[i] = [False] * u
+        elif kind == "epilogue":
+            for p in range(u):
+                assert not ounread[p][i], f"rank {i} overwrote {p}'s O chunk before it was unpacked"
+                orecv[p][i], ounread[p][i] = a, True
+        elif kind == "unpack_out":
+            assert all(orecv[i][p] == a for p in range(u)), "unpacked an O chunk of another call"
+            ounread[i] = [False] * u
+        pc[i] += 1
+        return True
+
+    while True:
+        order = list(range(u))
+        rng.shuffle(order)
+        if not any(step(i) for i in order):
+            break
+    assert pc == [len(p) for p in prog], f"deadlock: {pc}"
+    assert all(v == 0 for f in flags for v in f.values())
+
+
+@pytest.mark.parametrize("u", [2, 3, 4, 8])
+def test_ulysses_flag_protocol(u):
+    for seed in range(200):
+        simulate_ulysses(u, calls=3, seed=seed)
