@@ -1,0 +1,41 @@
+"""Host logic of bench.py (no GPU): the default mesh choice (CFG first, then the largest Ulysses degree
+dividing H -- P:414), the config object both arms print, and the algorithmic
+communication bytes per rank (Table 1)."""
+import argparse
+
+import bench
+from paper_2411_01738_b200 import usp
+from paper_2411_01738_b200.inputs import WORKLOADS
+
+
+def test_default_split():
+    assert bench.default_split(1, 24, 1) == (1, 1, 1)
+    assert bench.default_split(8, 24, 1) == (1, 8, 1)       # Flux: Ulysses 8 (24 % 8 == 0)
+    assert bench.default_split(8, 16, 1) == (1, 8, 1)       # PixArt
+    assert bench.default_split(8, 48, 2) == (2, 4, 1)       # CogVideoX: CFG 2 x USP 4
+    assert bench.default_split(1, 48, 2) == (1, 1, 1)       # one GPU: both CFG branches on it
+    assert bench.default_split(6, 24, 1) == (1, 6, 1)
+    c, u, r = bench.default_split(8, 12, 1)                 # 12 % 8 != 0: Ulysses 4, ring 2
+    assert (c, u, r) == (1, 4, 2)
+
+
+def test_reference_arm_prints_our_config():
+    for name in ("flux", "pixart", "cogvideox"):
+        a = argparse.Namespace(gpus=8, ulysses=0, ring=0, transport="peer")
+        cfg = bench.ours_config(a, WORKLOADS[name])
+        assert cfg["workload"] == name and cfg["cfg"] * cfg["ulysses"] * cfg["ring"] == 8
+        assert cfg["transport"] == "peer"
+    a = argparse.Namespace(gpus=1, ulysses=0, ring=0, transport="peer")
+    cfg = bench.ours_config(a, WORKLOADS["flux"])
+    assert cfg["transport"] is None and cfg["l2"] == "inputs larger than L2"
+
+
+def test_comm_bytes_match_table1():
+    """Flux N = 8: 177.5 MB (8x1), 253.6 MB (4x2), 405.8 MB (2x4), 710.2 MB (1x8)."""
+    w = WORKLOADS["flux"]
+    want = {(8, 1): 177.5e6, (4, 2): 253.6e6, (2, 4): 405.8e6, (1, 8): 710.2e6}
+    for (u, r), mb in want.items():
+        pl = usp.plan(w.B, w.H, w.S_txt, w.S_img, w.D, u, r, 0)
+        got = bench.comm_summary(pl, w.B, w, u, r, 1.0)["bytes_per_rank"]
+        assert abs(got - mb) / mb < 0.01, (u, r, got, mb)
+    assert bench.comm_summary(usp.plan(1, 24, 512, 65536, 128, 1, 1, 0), 1, w, 1, 1, 1.0) is None
