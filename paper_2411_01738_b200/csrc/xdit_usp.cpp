@@ -666,7 +666,7 @@ extern "C" {
 
 const char* xdit_last_error(void) { return g_err.c_str(); }
 
-int xdit_version(void) { return 101; }
+int xdit_version(void) { return 20000; }  // 2.0.0: xdit_rowmap gained the segment table (ABI break)
 
 uint64_t xdit_launch_count(void) { return xdit::g_launches.load(std::memory_order_relaxed); }
 
