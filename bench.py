@@ -7,20 +7,25 @@
 A "step" is one USP attention call (pack -> all-to-all -> ring of tcgen05
 attention + LSE merge -> reverse all-to-all) over one batch of synthetic Q/K/V of the workload.
 N=1 default workload: Flux.1 4096px (B=1, H=24, D=128, 512 text + 65536 image tokens), the shape
-BASELINE.json's north_star targets.  Multi-GPU: one process per GPU under
-torchrun (torch.distributed/NCCL for the barrier and the max over ranks); the library moves the USP
-bytes itself (peer-memory transport, or NCCL with --transport nccl); the same global problem is
-split over N ranks (strong scaling), CFG groups when the workload has them.  Rank 0 prints ONE JSON
-line.  XDIT_SHARE_GPU=1 puts every rank on cuda:0 with a gloo process group -- a functional check of
-the N > 1 path on a 1-GPU box (its timings are not scaling numbers).
+BASELINE.json's north_star targets.
+
+Multi-GPU: one process per GPU.  `--gpus N` with N > 1 started without torchrun re-launches itself
+under torch.distributed.run (N local ranks, 127.0.0.1); under torchrun WORLD_SIZE must equal
+--gpus.  The ranks form an NCCL process group; the library splits its communicator (Ulysses rows,
+Ring columns) and moves every USP byte over NCCL.  The same global problem is split over the N ranks
+(strong scaling), CFG groups first when the workload has them.  T(1) -- the same whole-job problem
+on one GPU -- is measured in the same job by rank 0, so the line carries the parallel efficiency
+T(1) / (N T(N)).  Rank 0 prints ONE JSON line.  `--share-gpu` runs N ranks on cuda:0 (each rank a
+distinct NCCL host id, socket transport): a functional check of the N > 1 path on a 1-GPU box whose
+timings are not scaling numbers.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import statistics
+import subprocess
 import sys
 import threading
 import time
@@ -31,10 +36,11 @@ sys.path.insert(0, ROOT)
 METRIC = "USP attention TFLOP/s & ms/layer at 1/2/4/8 B200; % of bf16 tensor peak"
 UNIT = "TFLOP/s"
 DATASHEET_BF16_TFLOPS = 2250.0
+NVLINK_GBPS_PER_DIR = 900.0
 L2_BYTES = 126 * 1024 * 1024
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -43,20 +49,14 @@ def parse():
     ap.add_argument("--ulysses", type=int, default=0)
     ap.add_argument("--ring", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
-                    help="multi-rank byte movement: the library's peer-memory transport or NCCL")
+    ap.add_argument("--share-gpu", action="store_true",
+                    help="N > 1 ranks on cuda:0 (functional check on a 1-GPU box; not a scaling number)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-t1", action="store_true", help="N > 1: skip the same-job T(1) measurement")
     ap.add_argument("--no-graph", action="store_true",
                     help="N > 1: time eager calls instead of replaying the step captured in a CUDA graph")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU time of the oracle sample")
-    return ap.parse_args()
-
-
-def attn_kernel_name(D: int) -> str:
-    """The bf16 attention kernel the library dispatches for head dim D (attn_fwd_sm100.cu)."""
-    if D in (64, 72, 128) and os.environ.get("XDIT_ATTN_KERNEL") != "1sm":
-        return "attn_fwd_2sm_kernel"
-    return "attn_fwd_sm100_kernel"
+    return ap.parse_args(argv)
 
 
 def peaks():
@@ -75,6 +75,77 @@ def default_split(N: int, H: int, cfg: int):
     sp = N // c
     u = max(d for d in range(1, sp + 1) if sp % d == 0 and H % d == 0)
     return c, u, sp // u
+
+
+def split_for(args, w):
+    cfg, u, r = default_split(args.gpus, w.H, w.cfg)
+    if args.ulysses or args.ring:
+        u = args.ulysses or max(1, args.gpus // cfg // max(1, args.ring))
+        r = args.ring or max(1, args.gpus // cfg // u)
+    return cfg, u, r
+
+
+def ours_config(args, w):
+    """The `config` object both arms print for the same launch (the reference arm prints it too, so
+    the two lines name one workload)."""
+    cfg, u, r = split_for(args, w)
+    sp = u * r
+    B = w.B * w.cfg // cfg
+    L = w.S // sp + (1 if w.S % sp else 0)
+    flush = 4 * B * L * w.H * w.D * 2 < 2 * L2_BYTES
+    return {"workload": w.name, "B": w.B * w.cfg, "H": w.H, "D": w.D, "S_txt": w.S_txt, "S_img": w.S_img,
+            "cfg": cfg, "ulysses": u, "ring": r, "data_plane": "nccl" if args.gpus > 1 else None,
+            "l2": "flushed between steps" if flush else "inputs larger than L2"}
+
+
+def comm_summary(pl, B: int, w, u: int, r: int, ms: float):
+    """Algorithmic bytes this rank sends per call (SURVEY §8(d); Table 1, P:338-346): the Ulysses
+    Q,K,V exchange and the O (+LSE) return to the u-1 peers, and r-1 ring steps of K,V; and the time
+    they take at NVLink 5's 900 GB/s per direction -- the share of the call a perfectly overlapped
+    data plane would need (the Ulysses part is not overlapped)."""
+    if u * r == 1:
+        return None
+    a2a = (u - 1) * pl.a2a_bytes_per_peer  # Q, K, V to the u-1 peers
+    o_ret = (u - 1) * (B * pl.Lmax * pl.Hh * w.D * 2 + B * pl.Hh * pl.Lmax * 4) if u > 1 else 0
+    ring = sum(pl.ring_bytes[s] for s in range(r))
+    tot = a2a + o_ret + ring
+    return {"bytes_per_rank": int(tot), "ulysses_bytes": int(a2a + o_ret), "ring_bytes": int(ring),
+            "ms_at_900GBps": tot / (NVLINK_GBPS_PER_DIR * 1e9) * 1e3,
+            "share_of_call_at_900GBps": tot / (NVLINK_GBPS_PER_DIR * 1e9) * 1e3 / ms}
+
+
+def phase_summary(phs):
+    """Per-phase times (max over ranks) and the achieved NVLink-direction bandwidth of each exchange:
+    the bytes a rank sends in the phase / the phase's time, against 900 GB/s per direction."""
+    if not phs or any(p is None for p in phs):
+        return None
+    r = len(phs[0]["attn_ms"])
+    mx = lambda key: max(p[key] for p in phs)  # noqa: E731
+    out = {"ranks": len(phs), "total_ms": mx("total_ms"), "a2a_in_ms": mx("a2a_in_ms"),
+           "a2a_out_ms": mx("a2a_out_ms"),
+           "attn_ms": [max(p["attn_ms"][s] for p in phs) for s in range(r)],
+           "ring_comm_ms": [max(p["ring_comm_ms"][s] for p in phs) for s in range(r - 1)]}
+
+    def gbps(b, ms):
+        return b / (ms * 1e-3) / 1e9 if ms > 0 else None
+    p0 = phs[0]
+    bw = {}
+    if p0["a2a_in_bytes"]:
+        g = gbps(p0["a2a_in_bytes"], out["a2a_in_ms"])
+        bw["a2a_in"] = {"bytes_per_rank": p0["a2a_in_bytes"], "GBps": g, "frac_of_900": g / NVLINK_GBPS_PER_DIR,
+                        "note": "phase time includes the pack and unpack kernels"}
+    if p0["a2a_out_bytes"]:
+        g = gbps(p0["a2a_out_bytes"], out["a2a_out_ms"])
+        bw["a2a_out"] = {"bytes_per_rank": p0["a2a_out_bytes"], "GBps": g, "frac_of_900": g / NVLINK_GBPS_PER_DIR,
+                         "note": "phase time includes the unpack kernels"}
+    if r > 1:
+        rb, rt = sum(p0["ring_bytes"]), sum(out["ring_comm_ms"])
+        g = gbps(rb, rt)
+        bw["ring"] = {"bytes_per_rank": rb, "GBps": g, "frac_of_900": g / NVLINK_GBPS_PER_DIR,
+                      "hidden_under_attention": rt <= sum(out["attn_ms"]),
+                      "note": "side-stream send/recv time, overlapped with the attention kernel (P:356)"}
+    out["bandwidth"] = bw
+    return out
 
 
 # ------------------------------------------------------------------------------------ clocks
@@ -135,125 +206,133 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------------ CPU oracle
-def oracle_sample(w, seconds: float, rank_seed: int = 0):
-    """Time the fp64 oracle (as it stands) on a bounded row sample of workload `w` on the host cores.
-    Returns (flops_per_second, cores, description)."""
+def cpu_baseline_leg(w, seconds: float, q_rows, k_heads, v_heads, rows_desc: str, got=None):
+    """The cpu_baseline leg: the fp64 oracle, as it stands, on the host cores, on a bounded sample of
+    the workload -- query rows x heads of the benched inputs (q_rows [B, n, h, D], k/v_heads
+    [B, S, h, D], host tensors) -- sized to ~`seconds` of CPU time.  Timed on the sample and scaled to
+    TFLOP/s.  When `got` = (O [B, n, h, D], LSE [B, h, n]) of the benched GPU call on the same rows x
+    heads is given, the same oracle rows are the parity check of the benched run (§8(d) result
+    record).  Returns (cpu_baseline dict, parity dict or None)."""
     import numpy as np
     import oracle
-    rng = np.random.default_rng(rank_seed)
-    S, D = w.S, w.D
-    # one (b, h) slice of the global problem: K, V of all S keys, a strided sample of query rows
-    k = rng.standard_normal((1, S, 1, D))
-    v = rng.standard_normal((1, S, 1, D))
-    q = rng.standard_normal((1, S, 1, D))
+    f = lambda t: t.to("cpu").double().numpy()  # noqa: E731
+    K, V = f(k_heads), f(v_heads)
+    Qall = f(q_rows)
+    B, n_all, h, D = Qall.shape
+    S = K.shape[1]
     cores = oracle.default_threads()
-    per_row = 4.0 * S * D
-    n = max(cores, 8)
+    per_row = 4.0 * S * D * h * B
+    n = min(n_all, max(cores, 8))
     while True:  # calibrate: grow the sample until it costs >= 1/4 of the target
-        rows = np.linspace(0, S - 1, n).astype(np.int64)
         t0 = time.perf_counter()
-        oracle.attention_rows(q, k, v, rows)
+        oracle.attention(Qall[:, :n], K, V)
         dt = time.perf_counter() - t0
-        if dt >= seconds / 4 or n >= S:
+        if dt >= seconds / 4 or n >= n_all:
             break
-        n = min(S, int(n * max(2.0, (seconds / 4) / max(dt, 1e-3))))
-    # final timed run at the target size
-    n = min(S, max(n, int(n * seconds / max(dt, 1e-3))))
-    rows = np.linspace(0, S - 1, n).astype(np.int64)
+        n = min(n_all, int(n * max(2.0, (seconds / 4) / max(dt, 1e-3))))
+    n = min(n_all, max(n, int(n * seconds / max(dt, 1e-3))))
     t0 = time.perf_counter()
-    oracle.attention_rows(q, k, v, rows)
+    ref_o, ref_l = oracle.attention(Qall[:, :n], K, V)
     dt = time.perf_counter() - t0
-    desc = (f"{n} query rows x 1 (batch, head) of {w.name} (S={S}, D={D}) in fp64, "
-            f"{dt:.1f}s; rate scaled to the full 4*B*H*S^2*D workload")
-    return n * per_row / dt, cores, desc, dt
-
-
-def ours_config(args, w):
-    """The `config` object our arm prints for the same launch (so both lines name one workload)."""
-    N = args.gpus
-    cfg, u, r = default_split(N, w.H, w.cfg)
-    if args.ulysses or args.ring:
-        u = args.ulysses or max(1, N // cfg // max(1, args.ring))
-        r = args.ring or max(1, N // cfg // u)
-    sp = u * r
-    B = w.B * w.cfg // cfg
-    L = w.S // sp + (1 if w.S % sp else 0)
-    flush = 4 * B * L * w.H * w.D * 2 < 2 * L2_BYTES
-    return {"workload": w.name, "B": w.B * w.cfg, "H": w.H, "D": w.D, "S_txt": w.S_txt, "S_img": w.S_img,
-            "cfg": cfg, "ulysses": u, "ring": r, "transport": args.transport if sp > 1 else None,
-            "l2": "flushed between steps" if flush else "inputs larger than L2"}
-
-
-def comm_summary(pl, B: int, w, u: int, r: int, ms: float):
-    """Algorithmic bytes this rank sends per call (SURVEY §8(d); Table 1, P:338-346): the Ulysses
-    Q,K,V exchange and the O (+LSE) return to the u-1 peers, and r-1 ring steps of K,V; and the time
-    they take at NVLink 5's 900 GB/s per direction -- the share of the call a perfectly overlapped
-    transport would need (the Ulysses part is not overlapped)."""
-    if u * r == 1:
-        return None
-    a2a = (u - 1) * pl.a2a_bytes_per_peer  # Q, K, V to the u-1 peers
-    o_ret = (u - 1) * (B * pl.Lmax * pl.Hh * w.D * 2 + B * pl.Hh * pl.Lmax * 4) if u > 1 else 0
-    ring = sum(pl.ring_bytes[s] for s in range(r))
-    tot = a2a + o_ret + ring
-    return {"bytes_per_rank": int(tot), "ulysses_bytes": int(a2a + o_ret), "ring_bytes": int(ring),
-            "ms_at_900GBps": tot / 900e9 * 1e3, "share_of_call_at_900GBps": tot / 900e9 * 1e3 / ms}
+    cpu = {"value": n * per_row / dt / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle",
+           "sample": f"{n} query rows x {h} heads x B={B} of {w.name} (S={S}, D={D}; {rows_desc}) in fp64, "
+                     f"{dt:.1f}s on the host cores; rate scaled to TFLOP/s"}
+    par = None
+    if got is not None:
+        go, gl = f(got[0])[:, :n], f(got[1])[:, :, :n]
+        d = go - ref_o
+        par = {"err_O_maxabs": float(np.abs(d).max()),
+               "err_O_relL2": float(np.linalg.norm(d) / np.linalg.norm(ref_o)),
+               "err_LSE_maxabs": float(np.abs(gl - ref_l).max()),
+               "oracle_rows_checked": int(n * h * B),
+               "gates": {"O_maxabs": 2e-2, "LSE_maxabs": 1e-3, "O_relL2_internal": 1e-2, "LSE_internal": 1e-4}}
+        par["pass"] = bool(par["err_O_maxabs"] <= 2e-2 and par["err_LSE_maxabs"] <= 1e-3 and
+                           par["err_O_relL2"] <= 1e-2)
+    return cpu, par
 
 
 def run_reference(args, w, rank: int):
+    """The baseline arm for this tier: the fp64 oracle as it stands, on the host cores (rank 0 only),
+    each step a bounded row sample of the workload; ms_per_step is extrapolated from the sample."""
     if rank != 0:
         return 0
+    import torch
+    from paper_2411_01738_b200.inputs import qkv, seed_for
     flops_step = w.flops()
-    rates = []
+    rates, desc = [], None
     per_step = max(2.0, args.cpu_seconds / max(1, args.steps))
+    gen_S = w.S
+    gq, gk, gv = qkv(1, gen_S, 1, w.D, seed=seed_for(w, 0))  # one (batch, head) of the global problem
+    rows = torch.linspace(0, gen_S - 1, min(gen_S, 4096)).long()
     for it in range(args.warmup + args.steps):
-        rate, cores, desc, dt = oracle_sample(w, per_step if it >= args.warmup else 1.0, rank_seed=it)
+        cpu, _ = cpu_baseline_leg(w, per_step if it >= args.warmup else 1.0, gq[:, rows], gk, gv,
+                                  "one (b, h) slice, strided rows")
         if it >= args.warmup:
-            rates.append(rate)
-    rate = statistics.median(rates)
-    tflops = rate / 1e12
+            rates.append(cpu["value"])
+            desc = cpu
+    tflops = statistics.median(rates)
     line = {
         "impl": "reference", "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": flops_step / rate * 1e3,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": flops_step / (tflops * 1e12) * 1e3,
+        "extrapolated": True, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": ours_config(args, w),
-        "cpu_baseline": {"value": tflops, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc},
+        "cpu_baseline": {**desc, "value": tflops},
         "e2e": {"value": tflops, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-# ------------------------------------------------------------------------------------ GPU arm
-def main():
-    args = parse()
+# ------------------------------------------------------------------------------------ launch
+def relaunch_under_torchrun(args, argv):
+    """`--gpus N` (N > 1) without torchrun: one process per GPU via torch.distributed.run."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + argv
+    return subprocess.call(cmd)
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
     from paper_2411_01738_b200.inputs import WORKLOADS
     w = WORKLOADS[args.config]
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    env_world = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and env_world is None:
+        return relaunch_under_torchrun(args, argv)
+    world = int(env_world or "1")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: launch one process per GPU")
     if args.impl == "reference":
         return run_reference(args, w, rank)
 
     import torch
     import torch.distributed as dist
+
     from paper_2411_01738_b200 import usp
     from paper_2411_01738_b200.inputs import qkv, seed_for
 
     N = world
-    share = os.environ.get("XDIT_SHARE_GPU") == "1"
-    if share:
-        local = 0
+    if N > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")          # NCCL init lines on stderr: ranks, devices,
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")   # bus ids, transports (the driver can check N)
+        if args.share_gpu:
+            os.environ["NCCL_HOSTID"] = f"xdit-bench-rank-{rank}"
+            os.environ.setdefault("NCCL_SOCKET_IFNAME", "lo")
+            local = 0
+        elif torch.cuda.device_count() < N:
+            raise SystemExit(f"bench.py: --gpus {N} needs {N} GPUs, this node has {torch.cuda.device_count()} "
+                             "(--share-gpu runs a functional check on one)")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if N > 1:
-        if share:
-            dist.init_process_group("gloo")
-        else:
-            dist.init_process_group("nccl", device_id=dev)
-    cfg, u, r = default_split(N, w.H, w.cfg)
-    if args.ulysses or args.ring:
-        u = args.ulysses or max(1, N // cfg // max(1, args.ring))
-        r = args.ring or max(1, N // cfg // u)
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, u, r = split_for(args, w)
     assert cfg * u * r == N, f"cfg*u*r = {cfg}*{u}*{r} != N={N}"
     sp = u * r
     cfg_group, sp_rank = rank // sp, rank % sp
@@ -263,7 +342,7 @@ def main():
         group = groups[cfg_group]
     # batch handled by this CFG group: CFG splits the 2-latent batch
     B = w.B * w.cfg // cfg
-    comm = usp.Comm(u, r, group=group if sp > 1 else None, transport=args.transport)
+    comm = usp.Comm(u, r, group=group if sp > 1 else None)
     comm.reserve(B, w.H, w.S_txt, w.S_img, w.D, 2)
     to, tl, io, il = usp.shard(w.S_txt, w.S_img, sp, sp_rank)
     L = tl + il
@@ -271,7 +350,6 @@ def main():
     gq, gk, gv = qkv(B, w.S, w.H, w.D, seed=seed_for(w, cfg_group), device=dev)
     idx = torch.cat([torch.arange(to, to + tl), w.S_txt + torch.arange(io, io + il)]).to(dev)
     q, k, v = (t.index_select(1, idx).contiguous() for t in (gq, gk, gv))
-    del gq, gk, gv
     out = torch.empty_like(q)
     lse = torch.empty((B, w.H, L), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream()
@@ -287,20 +365,51 @@ def main():
     def max_over_ranks(x: float) -> float:
         if N == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cpu" if share else dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
+
+    def gather_obj(o):
+        if N == 1:
+            return [o]
+        allo = [None] * N
+        dist.all_gather_object(allo, o)
+        return allo
 
     working_set = 4 * q.numel() * q.element_size()
     flush = working_set < 2 * L2_BYTES
     scratch = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=dev) if flush else None
 
+    def timed(fn, steps):
+        """Mean ms of `steps` calls of fn on the device (CUDA events on the caller's stream, max over
+        ranks): back to back when the inputs exceed L2, else one call at a time after an L2 flush."""
+        if not flush:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier()
+            e0.record(stream)
+            for _ in range(steps):
+                fn()
+            e1.record(stream)
+            barrier()
+            return e0.elapsed_time(e1) / steps
+        tot = 0.0
+        for _ in range(steps):
+            scratch.fill_(1.0)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fn()
+            e1.record(stream)
+            barrier()
+            tot += e0.elapsed_time(e1)
+        return tot / steps
+
     for _ in range(args.warmup):
         step()
     barrier()
-    # N > 1: the step (a dozen kernels and stream flag operations per call) is captured once in a
-    # CUDA graph and replayed -- the peer transport's binary flags make replays valid -- so host
-    # enqueue cost does not pace the short multi-rank calls.  Falls back to eager calls if capture fails.
+    # N > 1: the step (a dozen kernels and NCCL operations per call) is captured once in a CUDA graph
+    # and replayed, so host enqueue cost does not pace the short multi-rank calls.  Falls back to
+    # eager calls if capture fails.
     graph, graph_note = None, None
     n_pre = usp.launch_count()
     if N > 1 and not args.no_graph:
@@ -323,62 +432,46 @@ def main():
     timed_step = graph.replay if graph is not None else step
     n0 = usp.launch_count()
     with ClockSampler(local) as clocks:
-        if not flush:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            barrier()
-            e0.record(stream)
-            for _ in range(args.steps):
-                timed_step()
-            e1.record(stream)
-            barrier()
-            ms = e0.elapsed_time(e1) / args.steps
-        else:  # small working set: flush L2 between steps, time each step on its own
-            tot = 0.0
-            for _ in range(args.steps):
-                scratch.fill_(1.0)
-                barrier()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                timed_step()
-                e1.record(stream)
-                barrier()
-                tot += e0.elapsed_time(e1)
-            ms = tot / args.steps
+        ms = timed(timed_step, args.steps)
     launches = (usp.launch_count() - n0) // args.steps
     if graph is not None:  # replays launch the captured kernels without passing through the library:
         launches = n_captured - n_pre  # the library's launches recorded into the graph (one call)
-
     ms = max_over_ranks(ms)
     flops = w.flops()  # whole job (all CFG groups)
     tflops = flops / (ms * 1e-3) / 1e12
 
-    # ---- dominant kernel alone: the tcgen05 attention kernel on this rank's ring-block shapes,
-    #      timed with events on the launching stream over K launches (roofline numerator)
+    # ---- per-phase events of the same calls (eager, profiled): the dominant kernel's time (the
+    #      attention launches of each ring step on the caller's stream) and the exchanges' bandwidth
+    comm.profile(True)
+    prof = []
+    for _ in range(max(3, min(args.steps, 10))):
+        if flush:
+            scratch.fill_(1.0)
+        barrier()
+        step()
+        prof.append(comm.phases())
+    comm.profile(False)
+    attn_ms = statistics.mean(sum(p["attn_ms"]) for p in prof)
+    phs = gather_obj(prof[-1])
+    phases = phase_summary(phs) if N > 1 else None
     pl = usp.plan(B, w.H, w.S_txt, w.S_img, w.D, u, r, sp_rank)
-    Hh, Sb = pl.Hh, pl.S_blk
-    kq = torch.empty((B, Sb, Hh, w.D), dtype=torch.bfloat16, device=dev).normal_()
-    kk, kv_ = torch.empty_like(kq).normal_(), torch.empty_like(kq).normal_()
-    ko = torch.empty_like(kq)
-    kl = torch.empty((B, Hh, Sb), dtype=torch.float32, device=dev)
-    kmap = usp.RowMap.plain(B, Sb, Hh, w.D)
-    kscr = torch.empty(usp.attn_scratch_bytes(w.D) // 4, dtype=torch.float32, device=dev)
+    kern_flops = sum(4.0 * B * pl.Hh * pl.S_blk * pl.ring_rows[s] * w.D for s in range(r))
+    kern_ms = max_over_ranks(attn_ms)
 
-    def kern():  # same launch configuration as inside the USP call (tail split enabled)
-        usp.attn_fwd(kq, kk, kv_, ko, kl, B=B, H=Hh, Sq=Sb, Skv=Sb, D=w.D,
-                     q_strides=(Sb * Hh * w.D, Hh * w.D, w.D), kv_strides=(Sb * Hh * w.D, Hh * w.D, w.D),
-                     omap=kmap, scratch=kscr)
-    for _ in range(2):
-        kern()
-    torch.cuda.synchronize()
-    k0, k1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    k0.record(stream)
-    for _ in range(args.steps):
-        kern()
-    k1.record(stream)
-    torch.cuda.synchronize()
-    kern_ms = max_over_ranks(k0.elapsed_time(k1) / args.steps)
-    kern_flops = 4.0 * B * Hh * Sb * Sb * w.D
-    del kq, kk, kv_, ko, kl
+    # ---- parity of the benched run + the cpu_baseline leg (rank 0: a sample of ITS rows / heads)
+    cpu, parity = None, None
+    if rank == 0 and not args.no_cpu_baseline:
+        rows_loc = torch.linspace(0, L - 1, min(L, 2048)).long()
+        hs = sorted({0, w.H // 2, w.H - 1})
+        hsel = torch.tensor(hs, device=dev)
+        q_rows = q[:, rows_loc.to(dev)].index_select(2, hsel)
+        got = (out[:, rows_loc.to(dev)].index_select(2, hsel), lse[:, :, rows_loc.to(dev)].index_select(1, hsel))
+        cpu, parity = cpu_baseline_leg(w, args.cpu_seconds if N == 1 else min(args.cpu_seconds, 5.0), q_rows,
+                                       gk.index_select(2, hsel), gv.index_select(2, hsel),
+                                       f"rank 0's rows, heads {hs}", got=got)
+        if N > 1:
+            cpu = None  # the CPU baseline is reported at N = 1 only; the parity check stays
+    del gq, gk, gv
 
     # ---- end to end through the public API with host buffers (pinned), copies inside the region
     hq, hk, hv = (t.cpu().pin_memory() for t in (q, k, v))
@@ -443,8 +536,6 @@ def main():
     e2e_streamed(2, g0)  # warm-up
     torch.cuda.synchronize()
     barrier()
-    # steady state of the copy/compute pipeline: the first step's H2D and the last D2H are not
-    # hidden, so they are amortised over 16 steps (all copies stay inside the timed region)
     n_stream = 16
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(stream)
@@ -457,32 +548,60 @@ def main():
     h2d = sum(t.numel() * t.element_size() for t in (hq, hk, hv))
     d2h = hout.numel() * hout.element_size() + hlse.numel() * hlse.element_size()
 
+    # ---- T(1): the same whole-job problem (every CFG group's batch) on ONE GPU, in this job (rank 0)
+    t1 = None
+    if N > 1 and not args.no_t1:
+        barrier()
+        if rank == 0:
+            Bt = w.B * w.cfg
+            parts = [qkv(w.B * w.cfg // cfg, w.S, w.H, w.D, seed=seed_for(w, c), device=dev) for c in range(cfg)]
+            q1, k1, v1 = (torch.cat([p[t] for p in parts], dim=0) for t in range(3))
+            del parts
+            o1 = torch.empty_like(q1)
+            l1 = torch.empty((Bt, w.H, w.S), dtype=torch.float32, device=dev)
+            big = 4 * q1.numel() * q1.element_size() >= 2 * L2_BYTES
+            with usp.Comm(1, 1) as c1:
+                def step1():
+                    usp.attention(q1, k1, v1, S_txt=w.S_txt, S_img=w.S_img, comm=c1, out=o1, lse=l1)
+                for _ in range(args.warmup):
+                    step1()
+                n1 = max(2, min(args.steps, 5))
+                tot = 0.0
+                for _ in range(1 if big else n1):  # inputs > L2: back to back; else flush + one call
+                    if not big:
+                        scratch.fill_(1.0)
+                    torch.cuda.synchronize()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record(stream)
+                    for _ in range(n1 if big else 1):
+                        step1()
+                    e1.record(stream)
+                    torch.cuda.synchronize()
+                    tot += e0.elapsed_time(e1)
+                t1 = tot / n1
+            del q1, k1, v1, o1, l1
+        barrier()
+
     peak, peak_sus, peak_src = peaks()
+    ranks = gather_obj({"rank": rank, "device": local, "pci_bus_id": torch.cuda.get_device_properties(dev).pci_bus_id
+                        if hasattr(torch.cuda.get_device_properties(dev), "pci_bus_id") else None,
+                        "name": torch.cuda.get_device_name(dev), "comm": comm.source})
     if rank == 0:
-        cpu = None
-        if not args.no_cpu_baseline and N == 1:
-            rate, cores, desc, _ = oracle_sample(w, args.cpu_seconds)
-            cpu = {"value": rate / 1e12, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+        kern_tflops = kern_flops / (kern_ms * 1e-3) / 1e12
         traffic = None
         try:
             with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-                tj = json.load(f)
-            key = f"{w.name}:{B}x{Hh}x{Sb}x{w.D}"
-            traffic = tj.get(key)
+                traffic = json.load(f).get(f"{w.name}:{B}x{pl.Hh}x{pl.S_blk}x{w.D}")
         except Exception:
             pass
-        kern_tflops = kern_flops / (kern_ms * 1e-3) / 1e12
+        share = args.share_gpu and N > 1
         line = {
             "metric": METRIC, "value": tflops, "unit": UNIT, "n_gpus": N, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": w.name, "B": w.B * w.cfg, "H": w.H, "D": w.D, "S_txt": w.S_txt,
-                       "S_img": w.S_img, "cfg": cfg, "ulysses": u, "ring": r,
-                       "transport": comm.transport if sp > 1 else None,
-                       "cuda_graph": graph is not None,
-                       **({"cuda_graph_note": graph_note} if graph_note else {}),
-                       **({"shared_gpu": True} if share and N > 1 else {}),
-                       "l2": "flushed between steps" if flush else "inputs larger than L2"},
+            "config": {**ours_config(args, w), **({"shared_gpu": True} if share else {})},
+            "cuda_graph": graph is not None,
+            **({"cuda_graph_note": graph_note} if graph_note else {}),
             "ms_per_layer": ms,
             "tflops_per_gpu": tflops / N,
             "pct_of_bf16_peak_measured": 100.0 * tflops / N / peak,
@@ -495,19 +614,29 @@ def main():
                     "serial": {"value": flops / (e2e_serial_ms * 1e-3) / 1e12, "ms_per_step": e2e_serial_ms,
                                "mode": "H2D, call, D2H back to back on one stream"}},
             "gpu_launches": int(launches),
-            "comm": comm_summary(pl, B, w, u, r, ms),
-            "roofline": {"bound": "tensor", "kernel": attn_kernel_name(w.D), "achieved": kern_tflops,
+            "parity": parity,
+            "roofline": {"bound": "tensor", "kernel": "attn_fwd_2sm_kernel", "achieved": kern_tflops,
                          "peak": peak, "unit": "TFLOP/s", "frac": kern_tflops / peak, "traffic": traffic,
                          "peak_source": f"{peak_src} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
                          "frac_of_sustained": kern_tflops / peak_sus,
+                         "frac_of_datasheet": kern_tflops / DATASHEET_BF16_TFLOPS,
                          "kernel_ms": kern_ms, "kernel_flops": kern_flops,
-                         "shape": f"B={B} H={Hh} Sq=Skv={Sb} D={w.D}"},
+                         "timing": "per-phase CUDA events of the benched calls (xdit_comm_profile): the attention "
+                                   "launches of every ring step on the caller's stream, mean of the profiled calls",
+                         "shape": f"B={B} H={pl.Hh} Sq={pl.S_blk} Skv={[pl.ring_rows[s] for s in range(r)]} D={w.D}"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }
+        if N > 1:
+            line["comm"] = comm_summary(pl, B, w, u, r, ms)
+            line["phases"] = phases
+            line["t1_ms"] = t1
+            line["parallel_efficiency"] = (t1 / (N * ms)) if t1 else None
+            line["ranks"] = ranks
+            line["nccl_version"] = ".".join(str(x) for x in torch.cuda.nccl.version())
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
-    if N > 1:  # peers may still map this rank's buffers: everyone drained before anyone frees
+    if N > 1:
         dist.barrier()
     comm.destroy()
     if N > 1:

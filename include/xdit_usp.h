@@ -55,15 +55,19 @@ typedef enum xdit_status {
   XDIT_ERR_ALIGNMENT = 6,     /* pointer not 16-byte aligned or row bytes not a multiple of 16 */
   XDIT_ERR_CUDA = 7,          /* a CUDA runtime/driver call failed (message has the name) */
   XDIT_ERR_NCCL = 8,          /* an NCCL call failed, or an async NCCL error was pending */
-  XDIT_ERR_WORKSPACE = 9,     /* problem exceeds the reservation made by xdit_comm_reserve */
-  XDIT_ERR_NOT_CONNECTED = 10 /* peer transport: workspace (re)reserved but not (re)connected */
+  XDIT_ERR_WORKSPACE = 9      /* problem exceeds the reservation made by xdit_comm_reserve */
 } xdit_status;
 
 /* Thread-local, NUL-terminated message for the last non-OK return ("" if none).  Valid until the
  * next call on the same thread.  Never NULL. */
 XDIT_API const char* xdit_last_error(void);
 
-/* Library ABI version (major*10000 + minor*100 + patch). */
+/* Library ABI version (major*10000 + minor*100 + patch).  A caller compiled against this header
+ * must check xdit_version() == XDIT_ABI_VERSION before passing any struct (xdit_rowmap, xdit_plan,
+ * xdit_p2p_op, xdit_phases) across the boundary: the layouts are fixed per ABI version.
+ * 3.0.0: NCCL is the only data plane (the round-1 peer-memory transport and its mailbox are gone,
+ * xdit_rowmap lost its segment table); xdit_p2p, per-phase timing, the KV-buffer call. */
+#define XDIT_ABI_VERSION 30000
 XDIT_API int xdit_version(void);
 
 /* Number of CUDA kernels this library has launched in this process (all devices, monotonic).
@@ -85,9 +89,13 @@ XDIT_API int xdit_usp_shard(int S_txt, int S_img, int nranks, int g, int* txt_of
 
 /* ------------------------------------------------------------------------------------------ */
 /* Communicators.  One handle per SP group (= one CFG group).  Mesh (reading C6): SP rank  */
-/* g = i*ulysses + j, i = ring index (SP-Ring column), j = Ulysses index (SP-Ulysses row).  The  */
-/* handle owns two NCCL sub-communicators split from the SP communicator: Ulysses (color i,     */
-/* key j) and Ring (color j, key i), plus all workspace.                                        */
+/* g = i*ulysses + j, i = ring index (SP-Ring column), j = Ulysses index (SP-Ulysses row).  Every  */
+/* byte between ranks moves over NCCL (NVLink / NVSwitch between the GPUs of one node): the handle */
+/* splits the SP communicator into the Ulysses row (color i, key j), the Ring column (color j,     */
+/* key i) and a private copy of the whole group (point-to-point messages, all-gathers), and owns   */
+/* all workspace.  Collectives and sends/receives run on an internal high-priority side stream     */
+/* joined to the caller's stream with events, or on the caller's stream itself; no call of the hot */
+/* path synchronises the host.                                                                     */
 /* ------------------------------------------------------------------------------------------ */
 
 /* Writes a fresh NCCL unique id (an opaque 128-byte blob) to id_out (HOST memory, >=128 bytes).
@@ -96,87 +104,56 @@ XDIT_API int xdit_usp_shard(int S_txt, int S_img, int nranks, int g, int* txt_of
 XDIT_API int xdit_nccl_unique_id(void* id_out);
 
 /* Collective over the nranks = ulysses*ring ranks of one SP group: builds the SP communicator
- * from `unique_id` (HOST, 128 bytes) on the current CUDA device, then splits the Ulysses and
- * Ring sub-communicators.  With nranks == 1, unique_id may be NULL and no NCCL object is made.
+ * from `unique_id` (HOST, 128 bytes) on the current CUDA device, then splits the sub-communicators.
+ * With nranks == 1, unique_id may be NULL and no NCCL object is made.
  * Errors: INVALID_ARG, COMM_MISMATCH (ulysses*ring != nranks), NCCL, CUDA. */
 XDIT_API int xdit_comm_init(const void* unique_id, int nranks, int rank, int ulysses, int ring,
                    xdit_comm_t* out);
 
-/* Same as xdit_comm_init but wraps an existing ncclComm_t of the SP group (for example one a
- * framework already owns, NCCL 2.28.x ABI).  The handle does not take ownership of nccl_comm.
- * nccl_comm may be NULL only when ulysses*ring == 1. */
+/* Same as xdit_comm_init but splits an existing ncclComm_t of the SP group -- the communicator a
+ * framework already owns, e.g. torch ProcessGroupNCCL's `_comm_ptr()` (torch bundles NCCL 2.28.x,
+ * the version this library links).  Collective over that communicator.  The handle never issues
+ * work on nccl_comm itself (only on the communicators split from it) and does not take ownership.
+ * nccl_comm may be NULL only when ulysses*ring == 1.  Errors: INVALID_ARG, COMM_MISMATCH, NCCL, CUDA. */
 XDIT_API int xdit_comm_create(void* nccl_comm, int ulysses, int ring, xdit_comm_t* out);
 
-/* ---- Peer-memory transport (no NCCL).  Same mesh and call semantics; the bytes move through
- * device memory the ranks map into each other (CUDA IPC; NVLink/NVSwitch peer mappings between
- * GPUs): the Ulysses pack kernel stores each head block straight into the owning peer's receive
- * buffer (pack + all-to-all in one kernel), ring K/V blocks are copied peer-to-peer into
- * the next rank's free slot while the attention kernel runs (Table 1 "overlapped"),
- * and the final epilogue stores O/LSE rows straight into their token owners' receive buffers
- * (xdit_rowmap segment table).  Streams are ordered across ranks with
- * 32-bit flags in device memory (cuStreamWriteValue32 into the peer's flag after a system-wide
- * fence, cuStreamWaitValue32 >= on the local one): nothing spins on an SM and no host thread
- * waits, so xdit_usp_attention stays stream-ordered and CUDA-graph capturable (the flags are binary:
- * the writer sets 1, the owner waits for 1 and resets 0 before the writer can set it again, so a
- * captured call replays correctly; the mailbox and the peer cfg_tail use epochs and are not
- * capturable), and several ranks may
- * share one GPU (one process per rank; ranks in one process are rejected).
- *
- * Setup, collective over the SP group (every rank, same order):
- *   xdit_comm_init_peer -> xdit_comm_reserve -> xdit_comm_peer_export (each rank's blob)
- *   -> exchange the blobs over any host channel (e.g. torch.distributed all_gather_object)
- *   -> xdit_comm_peer_connect(all nranks blobs, SP-rank order).
- * A reserve that reallocates the workspace clears the connection (the call then returns
- * NOT_CONNECTED) until export/exchange/connect is repeated.  All ranks must have drained their
- * streams before any rank reserves again or destroys its handle (e.g. synchronize + barrier).
- * Every rank must issue the same sequence of xdit_usp_attention calls on the handle (each call
- * advances a per-handle epoch that the flags carry). */
-enum { XDIT_TRANSPORT_NCCL = 0, XDIT_TRANSPORT_PEER = 1 };
-#define XDIT_PEER_BLOB_BYTES 1024
+/* ---- Point-to-point messages between ranks of a handle, for the patch activations PipeFusion
+ * passes between stages "via asynchronous P2P" (NEXT 3) and the boundary rows of the
+ * patch-parallel VAE (NEXT 4).  One call = one NCCL group of sends and receives on the
+ * handle's private communicator, enqueued on `stream` (no host synchronisation); every message is
+ * matched by the peer's op of the same size in ITS call, so any pattern in which each call's peers
+ * issue matching calls is deadlock-free.  buf: DEVICE memory, `bytes` long (0 allowed: no-op). */
+typedef struct xdit_p2p_op {
+  int32_t peer;     /* rank of the handle's group */
+  int32_t is_send;  /* 1 send buf to peer, 0 receive into buf from peer */
+  void* buf;
+  size_t bytes;
+} xdit_p2p_op;
+/* Errors: INVALID_ARG (NULL / peer out of range / n < 0), NCCL. */
+XDIT_API int xdit_p2p(xdit_comm_t comm, const xdit_p2p_op* ops, int n, xdit_stream_t stream);
 
-/* Creates a peer-transport handle for SP rank `rank` of nranks = ulysses*ring on the current CUDA
- * device (no communication).  Errors: INVALID_ARG, COMM_MISMATCH, UNSUPPORTED (the driver has no
- * stream memory operations), CUDA. */
-XDIT_API int xdit_comm_init_peer(int nranks, int rank, int ulysses, int ring, xdit_comm_t* out);
-
-/* Writes this rank's XDIT_PEER_BLOB_BYTES-byte descriptor (IPC handles of its receive buffers,
- * ring slots and flag words; HOST memory, caller-owned) to `blob`.  Call after xdit_comm_reserve.
- * Errors: INVALID_ARG (NULL, or not a peer handle), CUDA. */
-XDIT_API int xdit_comm_peer_export(xdit_comm_t comm, void* blob);
-
-/* Maps the buffers this rank writes into (Ulysses peers' receive buffers, the ring successor's
- * KV slots, the flag words of both ring neighbours and all Ulysses peers).  `blobs`: HOST array of
- * nranks descriptors from xdit_comm_peer_export, in SP-rank order.  Replaces any earlier mapping
- * (device-synchronising).  Errors: INVALID_ARG, COMM_MISMATCH (a blob from another mesh or
- * position), UNSUPPORTED (two ranks in one process), CUDA (IPC mapping failed). */
-XDIT_API int xdit_comm_peer_connect(xdit_comm_t comm, const void* blobs);
-
-/* XDIT_TRANSPORT_NCCL or XDIT_TRANSPORT_PEER; -1 for NULL. */
-XDIT_API int xdit_comm_transport(xdit_comm_t comm);
-
-/* ---- Peer transport mailbox: point-to-point messages between any two ranks of the handle, for
- * the patch activations PipeFusion passes between stages "via asynchronous P2P" (NEXT 3) and
- * the CFG tail's gather (NEXT 2).  Every rank owns nranks regions of bytes_per_src bytes
- * (region s receives from rank s).  Like xdit_comm_reserve, growing the mailbox clears the
- * connection: export / exchange / connect again (all ranks, after a drained barrier).
- * Ordering is the caller's protocol of monotonically increasing 32-bit tags per (sender, receiver):
- *   sender:   [xdit_p2p_wait_ack(receiver, t-k)] -> xdit_p2p_put(receiver, ..., t)
- *   receiver: xdit_p2p_wait(sender, t) -> consume its region -> xdit_p2p_ack(sender, t)
- * All four are stream-ordered (peer copy + cuStreamWriteValue32 / cuStreamWaitValue32); tags compare
- * wraparound-safe (>=).  Errors: INVALID_ARG, NOT_CONNECTED, WORKSPACE (no or too small mailbox), CUDA. */
-XDIT_API int xdit_comm_mailbox_reserve(xdit_comm_t comm, size_t bytes_per_src);
-/* DEVICE address and size of this rank's region that receives from rank `src`. */
-XDIT_API int xdit_p2p_mailbox(xdit_comm_t comm, int src, void** ptr, size_t* bytes);
-/* Copy `bytes` from DEVICE `src` into rank dst's region for this rank at dst_off, then set this rank's
- * data flag on dst to `tag` -- ordered after all prior work of `stream`. */
-XDIT_API int xdit_p2p_put(xdit_comm_t comm, int dst, const void* src, size_t bytes, size_t dst_off, uint32_t tag,
-                          xdit_stream_t stream);
-/* Later work of `stream` waits until sender `src`'s data flag here is >= tag. */
-XDIT_API int xdit_p2p_wait(xdit_comm_t comm, int src, uint32_t tag, xdit_stream_t stream);
-/* Tell `sender` (after all prior work of `stream`) that its messages up to `tag` are consumed. */
-XDIT_API int xdit_p2p_ack(xdit_comm_t comm, int sender, uint32_t tag, xdit_stream_t stream);
-/* Later work of `stream` waits until `receiver` acknowledged tag (>=). */
-XDIT_API int xdit_p2p_wait_ack(xdit_comm_t comm, int receiver, uint32_t tag, xdit_stream_t stream);
+/* ---- Per-phase timing of xdit_usp_attention (SURVEY §5 "CUDA events per phase").  While
+ * profiling is enabled, each call records timing events at its phase boundaries (not inside a
+ * CUDA-graph capture, where they would be illegal: captured calls record nothing).  After the
+ * call, xdit_comm_phases waits for its last event (HOST-synchronising) and reports:
+ *   total_ms          : first to last event of the call (caller's stream)
+ *   a2a_in_ms         : Ulysses pack + all-to-all of Q,K,V + unpack (u > 1)
+ *   attn_ms[s]        : ring step s on the caller's stream: waiting for KV block s, attention
+ *                       (with the merge fused into its epilogue) -- s < ring
+ *   ring_comm_ms[s]   : the side stream's send/recv of the next KV block during step s (s < ring-1)
+ *   a2a_out_ms        : reverse all-to-all of O (+LSE) + unpack (u > 1)
+ *   *_bytes           : the bytes this rank SENT in that phase (Table 1 algorithmic bytes)
+ * valid = 0 if the last call recorded nothing. */
+typedef struct xdit_phases {
+  int32_t valid, ulysses, ring, pad_;
+  float total_ms, a2a_in_ms, a2a_out_ms, pad2_;
+  float attn_ms[8];
+  float ring_comm_ms[8];
+  int64_t a2a_in_bytes, a2a_out_bytes;
+  int64_t ring_bytes[8];
+} xdit_phases;
+XDIT_API int xdit_comm_profile(xdit_comm_t comm, int enable);
+XDIT_API int xdit_comm_phases(xdit_comm_t comm, xdit_phases* out);
 
 /* Allocates (or grows) the device workspace for a problem: Ulysses send/recv buffers, the
  * unpacked Q block, two ring KV slots, fp32 ring accumulators.  Call once per shape before the
@@ -224,7 +201,8 @@ XDIT_API int xdit_usp_plan(int B, int H, int S_txt, int S_img, int D, int ulysse
 /*                otherwise; the fp32 entry point takes any D in [1, 256]).                     */
 /* S_txt, S_img : GLOBAL text / image token counts of the joint sequence.                       */
 /* ulysses,ring : degrees; must equal the handle's; H % ulysses == 0 (DIVISIBILITY).             */
-/* stream       : caller's CUDA stream; an internal side stream carries NCCL and is joined back. */
+/* stream       : caller's CUDA stream; the ring's NCCL send/recv run on an internal side stream */
+/*                (joined back with events), the Ulysses exchanges on `stream`.                 */
 /* comm         : handle from xdit_comm_init/create, reserved for this shape (WORKSPACE).        */
 /*                                                                                              */
 /* Steps: pack Q,K,V by head block -> Ulysses all-to-all -> unpack to the ring    */
@@ -258,13 +236,36 @@ XDIT_API int xdit_usp_attention_kv(const void* q, const void* k, const void* v, 
                                    void* kv_keep, int B, int H, int S_txt, int S_img, int D, int ulysses,
                                    int ring, xdit_stream_t stream, xdit_comm_t comm);
 
+/* USP attention of one PipeFusion patch over a persistent KV buffer -- the attention of hybrid
+ * PipeFusion x SP (§4.1.4: "the KV involved in Attention
+ * computation on different devices within the SP group should be consistent"; R6).
+ * q, k, v, out, lse: this rank's local rows of the PATCH, exactly as in xdit_usp_attention with
+ *          S_txt / S_img the patch's joint token counts (text rides with patch 0).
+ * kv_buf : DEVICE [2][B][H/ulysses][S_buf][D] (K then V, head-major), this rank's Ulysses head block
+ *          j = rank % ulysses, the block's KV over the WHOLE sequence; caller-owned and persistent
+ *          across diffusion steps, rows in the tokens' global order.  The SP group's fresh K,V of
+ *          the patch -- received through the Ulysses all-to-all (its ring block) and the ring
+ *          rotation (the other r-1 ring blocks), "the intermediate results ... stored in each
+ *          device's KV Buffer" -- are written to their tokens' rows: the patch's text token
+ *          t to row txt_row + t, its image token t to row img_row + t; the other rows keep what
+ *          they hold (stale K,V of the previous step); then the local queries attend
+ *          over all S_buf rows.  Ranks of one head block therefore hold identical buffers, and the
+ *          buffer is the one-device PipeFusion buffer restricted to the head block.
+ * dtype  : 0 bf16 (tcgen05 kernel, D in {64,72,128}), 1 fp32 (SIMT kernel).
+ * Errors: as xdit_usp_attention, plus INVALID_ARG (kv_buf NULL, rows beyond S_buf). */
+XDIT_API int xdit_usp_attention_buf(const void* q, const void* k, const void* v, void* out, float* lse,
+                                    void* kv_buf, int B, int H, int S_txt, int S_img, int D, int ulysses,
+                                    int ring, int S_buf, int txt_row, int img_row, int dtype,
+                                    xdit_stream_t stream, xdit_comm_t comm);
+
 /* CFG-parallel step tail ("performs an Allgather operation on
  * the latent space results"; reading R3).
  * xdit_cfg_combine: out = eps_uncond + g * (eps_cond - eps_uncond) elementwise over n elements,
  *   computed in fp32 and rounded once (RNE) to dtype (0 bf16, 1 fp32).  All DEVICE buffers, 16-byte
  *   aligned, n a multiple of 8 (bf16) / 4 (fp32) (ALIGNMENT).  out may alias either input.
  * xdit_cfg_tail: the same after an NCCL all-gather of each rank's eps_local (n elements) over the
- *   handle's ranks, which must be exactly the 2 ranks of a cfg pair (COMM_MISMATCH otherwise):
+ *   handle's ranks, which must be exactly the 2 ranks of a cfg pair (COMM_MISMATCH otherwise;
+ *   CUDA-graph capturable):
  *   rank 0 contributes the conditional, rank 1 the unconditional prediction.  eps_gather: DEVICE
  *   scratch of 2*n elements (receives [eps_cond; eps_uncond]); eps_out receives the combination on
  *   both ranks.  Stream-ordered on `stream`; errors: INVALID_ARG, ALIGNMENT, NCCL, CUDA. */
@@ -285,19 +286,13 @@ XDIT_API int xdit_cfg_tail(const void* eps_local, void* eps_gather, void* eps_ou
  *   o + s*o_seg + b*o_b + (t - seg_off[s])*o_s + h*o_h + d
  * and its LSE (b, h, t) to  lse + s*l_seg + b*l_b + h*l_h + (t - seg_off[s]).
  * A single segment with o_seg = l_seg = 0 is a plain strided tensor.  This lets the final
- * epilogue write straight into the reverse all-to-all send buffer (one segment per Ulysses peer). */
+ * epilogue write straight into the reverse all-to-all send buffer (one segment per Ulysses peer),
+ * so the bf16 cast and the reverse pack (a8) cost no pass of their own. */
 typedef struct xdit_rowmap {
   int32_t nseg;
   int32_t seg_off[9];
   int64_t o_seg, o_b, o_s, o_h;
   int64_t l_seg, l_b, l_h;
-  /* seg_table != 0: segment s starts at element o_seg_off[s] (O) / l_seg_off[s] (LSE) from the base
-   * pointer instead of s*o_seg / s*l_seg -- the peer transport points each segment at its owner's
-   * receive buffer (any address of the flat device address space, e.g. an NVLink peer mapping), so
-   * the epilogue's stores ARE the reverse all-to-all. */
-  int64_t o_seg_off[8];
-  int64_t l_seg_off[8];
-  int32_t seg_table;
 } xdit_rowmap;
 
 /* Flash attention forward of one (Q block, KV block) pair -- SURVEY §8(a) step a6.
@@ -332,8 +327,8 @@ XDIT_API int xdit_lse_merge(float* o_acc, float* lse_acc, const float* o_s, cons
 
 /* Ulysses pack: x [B][L][H][D] (contiguous, elem_bytes each) ->
  * send[p][t][B][Lmax][H/u][D] for p in [0,u) with t = `slot` of `nslots`, i.e. head block p of
- * every local token into peer p's contiguous chunk.  Rows L..Lmax-1 are left untouched.
- * Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+ * every local token into peer p's contiguous chunk (u in [1, 8]).  Rows L..Lmax-1 are left untouched.
+ * Errors: INVALID_ARG (also u > 8), ALIGNMENT, CUDA. */
 XDIT_API int xdit_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u, int slot,
                   int nslots, int elem_bytes, xdit_stream_t stream);
 
@@ -386,6 +381,17 @@ XDIT_API size_t xdit_pf_block_workspace_bytes(int B, int n, int H, int D, int dt
 XDIT_API int xdit_pf_block(void* h, void* kv_buf, const float* w, void* work, size_t work_bytes, int B, int H, int S,
                            int off, int n, int D, int dtype, xdit_stream_t stream);
 
+/* The two halves of xdit_pf_block around the attention, for hybrid PipeFusion x SP, where the
+ * patch's attention is the USP call xdit_usp_attention_buf (NEXT 3; reading R6):
+ * xdit_pf_qkv     : q, k, v [B][n][H][D] <- h * wq, h * wk, h * wv (fp32 products, one rounding).
+ * xdit_pf_residual: h <- h + g * o, o [B][n][H][D] of h's dtype (the USP call's output).
+ * w: DEVICE fp32 [4][H][D] = (wq, wk, wv, g).  dtype 0 bf16 / 1 fp32; 16-byte aligned, D % 8 == 0.
+ * Errors: INVALID_ARG, ALIGNMENT, CUDA. */
+XDIT_API int xdit_pf_qkv(const void* h, const float* w, void* q, void* k, void* v, int B, int n, int H, int D,
+                         int dtype, xdit_stream_t stream);
+XDIT_API int xdit_pf_residual(void* h, const void* o, const float* w, int B, int n, int H, int D, int dtype,
+                              xdit_stream_t stream);
+
 /* Synthetic sampler step (reading R4): x <- x - sigma * eps over n elements (n % 8 == 0), DEVICE
  * buffers of dtype 0 (bf16) or 1 (fp32); fp32 math, one rounding.  Errors: INVALID_ARG, ALIGNMENT, CUDA. */
 XDIT_API int xdit_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype, xdit_stream_t stream);
@@ -394,8 +400,8 @@ XDIT_API int xdit_pf_sampler(void* x, const void* eps, int64_t n, float sigma, i
 /* patch-parallel VAE decode (§4.3; reading R5). */
 /* Devices hold row bands of the feature maps; before every conv a band receives one boundary row  */
 /* from each neighbour ("the exchange of the boundary data for convolutional operators";    */
-/* paper_2411_01738_b200/vae.py moves them through the peer-transport mailbox), so activation       */
-/* memory per device falls to ~1/N and the decode stays exact.                              */
+/* paper_2411_01738_b200/vae.py moves them with xdit_p2p over NCCL), so activation memory per      */
+/* device falls to ~1/N and the decode stays exact.                                         */
 /* ------------------------------------------------------------------------------------------ */
 
 /* One decoder conv on a row band: out = conv3x3(in) + b, zero padding in x only.

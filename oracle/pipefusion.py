@@ -31,12 +31,13 @@ Functions:
   replay_stamps(N, M, L, T, warmup)           -> {(s, m, l): stamps of all M patches' KV visible}
   serial_eps(x, W)                            -> eps of one full-sequence (synchronous) step
   pipefusion(x, W, T, M, warmup, sigma, S_txt, N=1, order="patch") -> x after T steps, per-step xs
+  hybrid(x, W, T, M, warmup, sigma, S_txt, u, r, naive=False) -> x, per-rank KV buffers
 """
 from __future__ import annotations
 
 import numpy as np
 
-from . import attention
+from . import attention, local_rows
 
 
 def patch_bounds(S_txt: int, S_img: int, M: int):
@@ -150,3 +151,73 @@ def pipefusion(x, W, T: int, M: int, warmup: int, sigma: float, S_txt: int, N: i
         x = x - sigma * eps
         xs.append(x.copy())
     return x, xs
+
+
+def hybrid(x, W, T: int, M: int, warmup: int, sigma: float, S_txt: int, u: int, r: int, naive: bool = False):
+    """Hybrid PipeFusion x SP (§4.1.4; R6), fp64, emulating
+    the SP group's u*r ranks and their per-rank KV buffers step by step.
+
+      * "The entire hidden state is first split into M patches along the sequence dimension, and each
+        patch is further split into sp_degree patches": rank g of the SP group holds, of every
+        item (a patch, or the whole sequence in a synchronous warmup step), the rows the in-context
+        shard rule gives it on the item's own [text; image] tokens (P:240, reading C5);
+      * USP (P:382-384): rank g = (i, j) = (g // u, g % u) computes the attention output of the query
+        rows of its ring block i (the rows of ranks i*u .. i*u+u-1) for its Ulysses head block j
+        (reading C7), against ITS OWN KV buffer of block l -- heads of block j, every sequence row;
+      * the buffers: before the attention of an item at block l, rank g writes the item's fresh K,V
+        into its buffer.  naive=False: "after communication of K and V in SP-Ulysses and SP-Ring, the
+        intermediate results ... are stored in each device's KV Buffer" -- the rank keeps the
+        K,V of every row of the item it received (all-to-all: its ring block; ring: the others), i.e.
+        all the item's rows, heads of block j.  naive=True: "standard SP", which discards
+        them -- the rank writes only the rows it holds itself, so the buffers of an SP group diverge.
+
+    The item order is the sequential (patch-major) definition of `pipefusion`; the pipeline order of
+    the stages does not change a patch's buffer contents (pinned for `pipefusion`).  Returns the
+    latent after T steps and the final buffers kv[g][l] = (K [B,S,H/u,D], V [B,S,H/u,D])."""
+    if warmup < 1:
+        raise ValueError("PipeFusion needs >= 1 warmup step to fill the KV buffers (P:282)")
+    x = np.array(x, np.float64)
+    B, S, H, D = x.shape
+    N, Hh, L = u * r, H // u, len(W)
+    if H % u:
+        raise ValueError("H % ulysses != 0 (P:541)")
+    P = patch_bounds(S_txt, S - S_txt, M)
+    kb = [[np.zeros((B, S, Hh, D)) for _ in range(L)] for _ in range(N)]
+    vb = [[np.zeros((B, S, Hh, D)) for _ in range(L)] for _ in range(N)]
+    for s in range(T):
+        items = [None] if s < warmup else list(range(M))
+        eps = np.empty_like(x)
+        for m in items:
+            if m is None:
+                base, it_txt, it_img, img_base = 0, S_txt, S - S_txt, S_txt
+            else:
+                o, n = P[m]
+                base, it_txt = o, (S_txt if m == 0 else 0)
+                it_img, img_base = n - it_txt, (S_txt if m == 0 else o)
+            # global rows of every rank's shard of the item (text shard, then image shard)
+            own = []
+            for g in range(N):
+                lr = local_rows(it_txt, it_img, N, g)
+                own.append(np.where(lr < it_txt, lr, lr - it_txt + img_base))
+            rows = np.concatenate(own)
+            h = x[:, rows].copy()                       # the item's hidden rows, in SP-shard order
+            pos = {int(t): k for k, t in enumerate(rows)}
+            for l, (wq, wk, wv, wg) in enumerate(W):
+                q, k, v = h * wq, h * wk, h * wv
+                for g in range(N):  # fresh K,V into each rank's buffer (its head block j)
+                    j = g % u
+                    keep = rows if not naive else own[g]
+                    kk = [pos[int(t)] for t in keep]
+                    kb[g][l][:, keep] = k[:, kk][:, :, j * Hh:(j + 1) * Hh]
+                    vb[g][l][:, keep] = v[:, kk][:, :, j * Hh:(j + 1) * Hh]
+                o_att = np.empty_like(h)
+                for g in range(N):  # rank (i, j): ring block i's queries x head block j
+                    i, j = g // u, g % u
+                    blk = np.concatenate([own[i * u + p] for p in range(u)])
+                    qq = [pos[int(t)] for t in blk]
+                    oo, _ = attention(q[:, qq][:, :, j * Hh:(j + 1) * Hh], kb[g][l], vb[g][l])
+                    o_att[:, qq, j * Hh:(j + 1) * Hh] = oo
+                h = h + wg * o_att
+            eps[:, rows] = h
+        x = x - sigma * eps
+    return x, [[(kb[g][l], vb[g][l]) for l in range(L)] for g in range(N)]

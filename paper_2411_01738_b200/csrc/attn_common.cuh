@@ -37,8 +37,8 @@ struct EpiParams {
   const float* acc_l_in;
   float* acc_l_out;
   xdit_rowmap acc_map;
-  int diag;  // profiling only (XDIT_DIAG): 1 = softmax does no math, 2 = also no MMA<-softmax wait
-  unsigned long long* trace;  // profiling only (XDIT_TRACE): per-iteration clock64 stamps of CTA 0
+  int diag;  // profiling builds only (-DXDIT_PROFILE): 1 = the softmax does no math (skeleton)
+  unsigned long long* trace;  // profiling builds only: per-iteration clock64 stamps of the first pair
 };
 
 __device__ __forceinline__ float u2f(uint32_t x) { return __uint_as_float(x); }

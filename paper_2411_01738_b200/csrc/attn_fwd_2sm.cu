@@ -1,13 +1,16 @@
 // attn_fwd_2sm.cu -- flash-attention forward on a CTA PAIR (cta_group::2) for B200 (sm_100a).
 //
-// Same operation as attn_fwd_sm100.cu (§4.1.1 / P:257 §4.1.2;
-// readings C1-C3, C10, R1): O = softmax(Q K^T / sqrt(D)) V and LSE for one (Q block, KV block).
+// The bf16 attention of the hot path (§4.1.1 / P:257 §4.1.2;
+// readings C1-C3, C10, R1): O = softmax(Q K^T / sqrt(D)) V and LSE for one (Q block, KV block),
+// with the ring's LSE merge (a7) and the bf16 cast + reverse-all-to-all pack (a8) fused into the
+// epilogue.
 //
-// Why a second kernel: in the one-CTA kernel the S_t / P_t TMEM columns alias,
-// so QK^T of the next key tile of a query tile cannot start before the P.V of the current one --
-// every step of a tile is a serial chain softmax -> PV -> QK^T, and the tensor core idles ~40 %
-// (profiles/r01_ncu_attn_flux.md).  Here the two SMs of a TPC run one 256-row work item together
-// with M = 256 MMAs, which frees TMEM for DOUBLE-BUFFERED S and P per SM:
+// Why a CTA pair: in a one-CTA kernel holding two query tiles the S_t / P_t TMEM
+// columns alias, so QK^T of the next key tile of a query tile cannot start before the P.V of the
+// current one -- every step of a tile is a serial chain softmax -> PV -> QK^T, and the tensor core
+// idled ~40 % (round 1's one-CTA kernel, profiles/r01_ncu_attn_flux.md; retired in round 2, in git
+// history).  Here the two SMs of a TPC run one 256-row work item together with M = 256 MMAs, which
+// frees TMEM for DOUBLE-BUFFERED S and P per SM:
 //   * CTA rank r owns query rows [128 r, 128 r + 128) of the item: its Q tile, its S/P/O in TMEM;
 //   * each CTA loads HALF of every K tile (keys [64 r, 64 r + 64)) and HALF of every V tile
 //     (head-dim columns [D/2 r, D/2 r + D/2)): the pair's MMAs read the other half from the peer SM,
@@ -44,11 +47,22 @@ constexpr int kKeys = 128;         // keys per step
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kRegsSoftmax = 216, kRegsOther = 72;  // setmaxnreg split of 384 x 168 registers
+// exp2 pairs (of every 8) the softmax evaluates with the FMA-pipe polynomial instead of MUFU.EX2.
+// Release builds: 0 (profiles/r01_bench_flux*.json: the polynomial draws more power in the
+// power-capped sustained run for no throughput gain).  A/B builds set it with -DXDIT_EXP_EMU=n.
+#ifndef XDIT_EXP_EMU
+#define XDIT_EXP_EMU 0
+#endif
+#ifdef XDIT_PROFILE
 constexpr int kTraceIters = 64, kTraceEv = 16;
-// profiling only (XDIT_TRACE): clock64 stamps of warp 0 / the MMA lane of the first CTA pair
+#endif
+// Profiling builds only (-DXDIT_PROFILE, tools/ab_attn.sh): clock64 stamps of warp 0 / the MMA lane
+// of the first CTA pair (XDIT_PROFILE_TRACE) and the softmax-free skeleton (XDIT_PROFILE_DIAG).
 __device__ __forceinline__ void stamp(const EpiParams& p, int j, int ev) {
+#ifdef XDIT_PROFILE
   if (p.trace && j < kTraceIters && blockIdx.x < 2 && (threadIdx.x & 31) == 0)
     p.trace[(blockIdx.x * kTraceIters + j) * kTraceEv + ev] = clock64();
+#endif
 }
 
 template <int D>
@@ -366,7 +380,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int j = c; j < n_kv; j += 2) {
       ptx::mbar_wait_cluster(&s_full[c], (j >> 1) & 1);
       ptx::tc_fence_after();
-      if (p.diag) {  // profiling only (XDIT_DIAG=1): hand the barriers back without softmax work
+#ifdef XDIT_PROFILE
+      if (p.diag) {  // profiling builds only: hand the barriers back without softmax work
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);
         if (j >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((j - 2) >> 1) & 1);
@@ -381,6 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         m_ref = m_used = 0.f;
         continue;
       }
+#endif
       uint32_t s0[32], s1[32], s2[32], s3[32];
       const uint32_t tS = tmem + lane_off + C::col_s(c);
       ptx::tmem_ld32(tS, s0);
@@ -581,12 +597,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
 template <int D, int EMU>
 cudaError_t launch_kernel(dim3 grid, const CUtensorMap* m, const EpiParams& p, cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
+  static DeviceFlags attr_set;  // cudaFuncSetAttribute done on device d
+  if (!attr_set.test()) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_2sm_kernel<D, EMU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          Cfg<D>::kSmemBytes);
     if (e != cudaSuccess) return e;
-    attr_set = true;
+    attr_set.set();
   }
   attn_fwd_2sm_kernel<D, EMU><<<grid, kThreads, Cfg<D>::kSmemBytes, st>>>(m[0], m[1], m[2], m[3], m[4], m[5], p);
   note_launches(1);
@@ -626,13 +642,9 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.acc_l_out = a.acc_l_out;
   p.acc_map = a.acc_map;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
-  static const int diag = [] {
-    const char* e = std::getenv("XDIT_DIAG");
-    return e ? std::atoi(e) : 0;
-  }();
-  p.diag = diag;
-  // Work items (256 query rows of one (batch, head)) run one per CTA pair; the last partial wave
-  // of pairs is split over key ranges as in the one-CTA kernel (DESIGN.md §7.1 "tail split").
+  // Work items (256 query rows of one (batch, head)) run one per CTA pair; when the items leave a
+  // partial last wave of pairs, its items are split over key ranges written as normalised fp32
+  // partials into the scratch and merged by tail_merge_kernel (DESIGN.md §7.1 "tail split").
   p.n_qt = (a.Sq + kRowsPerItem - 1) / kRowsPerItem;
   const int items = p.n_qt * a.H * a.B;
   p.n_full = items;
@@ -640,14 +652,8 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.kv_chunk = a.Skv;
   p.part = nullptr;
   int n_tail = 0;
-  static const int npairs = [] {
-    int dev = 0, n = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    return n / 2;
-  }();
-  static const bool no_split = std::getenv("XDIT_NO_TAIL_SPLIT") != nullptr;
-  if (a.scratch && !no_split && items > npairs && items % npairs) {
+  const int npairs = device_sm_count() / 2;
+  if (a.scratch && items > npairs && items % npairs) {
     const int rem = items % npairs, n_kv_tiles = (a.Skv + kKeys - 1) / kKeys;
     int ns = std::min(std::min(npairs / rem, 8), n_kv_tiles / 2);
     if (ns >= 2) {
@@ -664,27 +670,23 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     }
   }
   const dim3 grid(2 * (p.n_full + n_tail * p.n_split));
+#ifdef XDIT_PROFILE
+  // profiling builds: XDIT_PROFILE_DIAG=1 in the environment runs the softmax-free skeleton,
+  // XDIT_PROFILE_TRACE=1 prints the first pair's clock64 stamps after the launch
+  static const int diag = [] {
+    const char* e = std::getenv("XDIT_PROFILE_DIAG");
+    return e ? std::atoi(e) : 0;
+  }();
+  p.diag = diag;
   static unsigned long long* trace = [] {
     unsigned long long* t = nullptr;
-    if (std::getenv("XDIT_TRACE")) cudaMalloc(&t, sizeof(unsigned long long) * 2 * kTraceIters * kTraceEv);
+    if (std::getenv("XDIT_PROFILE_TRACE")) cudaMalloc(&t, sizeof(unsigned long long) * 2 * kTraceIters * kTraceEv);
     return t;
   }();
   p.trace = trace;
   if (trace) cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 2 * kTraceIters * kTraceEv, st);
-  static const int emu = [] {
-    const char* e = std::getenv("XDIT_EXP_EMU");
-    return e ? std::atoi(e) : -1;
-  }();
-  cudaError_t err;
-  // Default 0: every exp2 on MUFU.  The FMA-pipe polynomial (EMU of 8 column pairs) gained ~1 % in
-  // short runs but draws more power; in the sustained bench the kernel is power-capped and EMU=0
-  // held a higher SM clock (1627 vs 1545 MHz) and throughput (profiles/r01_bench_flux*.json).
-  switch (emu >= 0 ? emu : 0) {
-    case 0: err = launch_kernel<D, 0>(grid, m, p, st); break;
-    case 1: err = launch_kernel<D, 1>(grid, m, p, st); break;
-    case 3: err = launch_kernel<D, 3>(grid, m, p, st); break;
-    default: err = launch_kernel<D, 2>(grid, m, p, st); break;
-  }
+#endif
+  cudaError_t err = launch_kernel<D, XDIT_EXP_EMU>(grid, m, p, st);
   if (err == cudaSuccess && n_tail) {
     const int rows = n_tail * kRowsPerItem;
     tail_merge_kernel<D><<<(rows + 7) / 8, 256, 0, st>>>(p.part, n_tail, p.n_split, p.n_full, p.n_qt, a.H,
@@ -692,7 +694,8 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     note_launches(1);
     err = cudaGetLastError();
   }
-  if (trace) {  // profiling only: stamps of the first pair relative to the leader's first stamp
+#ifdef XDIT_PROFILE
+  if (trace) {  // stamps of the first pair relative to the leader's first stamp
     static unsigned long long h[2 * kTraceIters * kTraceEv];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
@@ -708,15 +711,18 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
         fprintf(stderr, "\n");
       }
   }
+#endif
   return err;
 }
 
 }  // namespace pair2
 }  // namespace
 
-bool attn_fwd_2sm_supports(int D) { return D == 128 || D == 64 || D == 72; }
+size_t attn_scratch_floats(int D) { return size_t(device_sm_count()) * kRowsPerItem * size_t(D + 1); }
 
-cudaError_t launch_attn_fwd_2sm(const AttnArgs& a, cudaStream_t st) {
+bool attn_fused_merge_supported(int D) { return D == 128 || D == 64 || D == 72; }
+
+cudaError_t launch_attn_fwd_bf16(const AttnArgs& a, cudaStream_t st) {
   if (a.Sq == 0 || a.B == 0) return cudaSuccess;
   switch (a.D) {
     case 128: return pair2::launch_d<128>(a, st);

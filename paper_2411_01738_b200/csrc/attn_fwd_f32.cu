@@ -92,12 +92,12 @@ __global__ void __launch_bounds__(kThreads)
 template <int DQ>
 cudaError_t launch_dq(const AttnArgs& a, cudaStream_t st) {
   const size_t smem = size_t(2) * kKeys * a.D * sizeof(float);
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr;
+  if (!attr.test()) {
     cudaError_t e = cudaFuncSetAttribute(attn_fwd_f32_kernel<DQ>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kKeys * 256 * 4);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.set();
   }
   dim3 grid((a.Sq + kRows - 1) / kRows, a.H, a.B);
   attn_fwd_f32_kernel<DQ><<<grid, kThreads, smem, st>>>(

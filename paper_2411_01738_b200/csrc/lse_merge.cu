@@ -69,9 +69,7 @@ cudaError_t launch_lse_merge(float* o_acc, float* lse_acc, const float* o_s, con
                              const xdit_rowmap* fmap, int fin_dtype, cudaStream_t st) {
   const int64_t nrows = int64_t(B) * S * Hh;
   if (nrows == 0) return cudaSuccess;
-  int dev = 0, nsm = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = device_sm_count();
   int64_t blocks = (nrows + kWarps - 1) / kWarps;
   const int64_t cap = int64_t(nsm) * 8;  // grid-stride beyond 8 CTAs per SM
   if (blocks > cap) blocks = cap;

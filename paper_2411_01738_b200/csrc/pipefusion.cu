@@ -23,12 +23,7 @@ namespace xdit {
 namespace {
 
 int pf_grid(int64_t n) {
-  static int nsm = [] {
-    int dev = 0, v = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
+  const int nsm = device_sm_count();
   const int64_t blocks = (n + 255) / 256;
   return int(blocks < int64_t(nsm) * 8 ? (blocks > 0 ? blocks : 1) : int64_t(nsm) * 8);
 }
@@ -92,9 +87,9 @@ __global__ void pf_prep_kernel(const T* __restrict__ h, const float* __restrict_
   }
 }
 
-// h <- h + g * o  (o fp32 [B][n][H][D])
-template <typename T>
-__global__ void pf_residual_kernel(T* __restrict__ h, const float* __restrict__ o, const float* __restrict__ g,
+// h <- h + g * o  (o [B][n][H][D]: fp32 from pf_block's attention, or h's dtype from the USP call)
+template <typename T, typename O>
+__global__ void pf_residual_kernel(T* __restrict__ h, const O* __restrict__ o, const float* __restrict__ g,
                                    int64_t n8, int HD) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
     const int c = int((i * 8) % HD);
@@ -104,6 +99,26 @@ __global__ void pf_residual_kernel(T* __restrict__ h, const float* __restrict__ 
 #pragma unroll
     for (int k = 0; k < 8; ++k) x[k] = fmaf(g[c + k], a[k], x[k]);
     st8(h + i * 8, x);
+  }
+}
+
+// q, k, v <- h * wq, h * wk, h * wv  (all [B][n][H][D]; the hybrid's USP call does the KV placement)
+template <typename T>
+__global__ void pf_qkv_kernel(const T* __restrict__ h, const float* __restrict__ w, T* __restrict__ q,
+                              T* __restrict__ k, T* __restrict__ v, int64_t n8, int HD) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n8; i += int64_t(gridDim.x) * blockDim.x) {
+    const int c = int((i * 8) % HD);
+    float x[8], y[8];
+    ld8(h + i * 8, x);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] = x[e] * w[c + e];
+    st8(q + i * 8, y);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] = x[e] * w[HD + c + e];
+    st8(k + i * 8, y);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) y[e] = x[e] * w[2 * HD + c + e];
+    st8(v + i * 8, y);
   }
 }
 
@@ -169,16 +184,17 @@ cudaError_t launch_pf_block(void* h, void* kv, const float* w, void* work, int B
   if (dtype == 0) {
     a.scratch = scratch;
     a.scratch_floats = attn_scratch_floats(D);
-    e = launch_attn_fwd_sm100(a, st);
+    e = launch_attn_fwd_bf16(a, st);
   } else {
     e = launch_attn_fwd_f32(a, st);
   }
   if (e != cudaSuccess) return e;
   if (dtype == 0)
-    pf_residual_kernel<__nv_bfloat16><<<pf_grid(n8), 256, 0, st>>>(static_cast<__nv_bfloat16*>(h), o, w + 3 * H * D,
-                                                                   n8, H * D);
+    pf_residual_kernel<__nv_bfloat16, float><<<pf_grid(n8), 256, 0, st>>>(static_cast<__nv_bfloat16*>(h), o,
+                                                                          w + 3 * H * D, n8, H * D);
   else
-    pf_residual_kernel<float><<<pf_grid(n8), 256, 0, st>>>(static_cast<float*>(h), o, w + 3 * H * D, n8, H * D);
+    pf_residual_kernel<float, float><<<pf_grid(n8), 256, 0, st>>>(static_cast<float*>(h), o, w + 3 * H * D, n8,
+                                                                  H * D);
   note_launches(1);
   return cudaGetLastError();
 }
@@ -191,6 +207,38 @@ cudaError_t launch_pf_sampler(void* x, const void* eps, int64_t n, float sigma, 
   else
     pf_sampler_kernel<float><<<pf_grid(n / 8), 256, 0, st>>>(static_cast<float*>(x), static_cast<const float*>(eps),
                                                              n / 8, sigma);
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pf_qkv(const void* h, const float* w, void* q, void* k, void* v, int B, int n, int H, int D,
+                          int dtype, cudaStream_t st) {
+  const int64_t n8 = int64_t(B) * n * H * D / 8;
+  if (n8 == 0) return cudaSuccess;
+  if (dtype == 0) {
+    using T = __nv_bfloat16;
+    pf_qkv_kernel<T><<<pf_grid(n8), 256, 0, st>>>(static_cast<const T*>(h), w, static_cast<T*>(q), static_cast<T*>(k),
+                                                  static_cast<T*>(v), n8, H * D);
+  } else {
+    pf_qkv_kernel<float><<<pf_grid(n8), 256, 0, st>>>(static_cast<const float*>(h), w, static_cast<float*>(q),
+                                                      static_cast<float*>(k), static_cast<float*>(v), n8, H * D);
+  }
+  note_launches(1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pf_residual(void* h, const void* o, const float* w, int B, int n, int H, int D, int dtype,
+                               cudaStream_t st) {
+  const int64_t n8 = int64_t(B) * n * H * D / 8;
+  if (n8 == 0) return cudaSuccess;
+  if (dtype == 0) {
+    using T = __nv_bfloat16;
+    pf_residual_kernel<T, T><<<pf_grid(n8), 256, 0, st>>>(static_cast<T*>(h), static_cast<const T*>(o), w + 3 * H * D,
+                                                          n8, H * D);
+  } else {
+    pf_residual_kernel<float, float><<<pf_grid(n8), 256, 0, st>>>(static_cast<float*>(h), static_cast<const float*>(o),
+                                                                  w + 3 * H * D, n8, H * D);
+  }
   note_launches(1);
   return cudaGetLastError();
 }

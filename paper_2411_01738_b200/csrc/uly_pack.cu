@@ -15,12 +15,11 @@ namespace xdit {
 namespace {
 
 template <typename V>
-__global__ void pack_kernel(const V* __restrict__ x, PeerDst dst, int B, int L, int Lmax, int H, int Hh,
+__global__ void pack_kernel(const V* __restrict__ x, ChunkDst dst, int B, int L, int Lmax, int H, int Hh,
                             int vpr /* vectors per (row, head) */, int u, int slot, int nslots) {
   // x [B][L][H][vpr] -> chunk of Ulysses peer p = h / Hh: dst.p[p] [slot][B][Lmax][Hh][vpr].
-  // dst.p[p] is either this rank's send buffer at chunk p (NCCL transport) or, with the peer-memory
-  // transport, peer p's receive buffer at this rank's chunk -- the stores then travel over NVLink
-  // and the pack IS the all-to-all (one kernel, no staging copy).
+  // dst.p[p] is this rank's send buffer at chunk p for the other Ulysses ranks, and its own receive
+  // buffer at chunk j for its own head block (which therefore never crosses NCCL).
   const int64_t n = int64_t(B) * L * H * vpr;
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n;
        i += int64_t(gridDim.x) * blockDim.x) {
@@ -100,7 +99,7 @@ __global__ void unpack_lse_kernel(const char* __restrict__ lrecv, int64_t peer_s
 
 unsigned grid_for(int64_t n, int threads) {
   int64_t g = (n + threads - 1) / threads;
-  const int64_t cap = 148 * 16;
+  const int64_t cap = int64_t(device_sm_count()) * 16;
   return unsigned(g < 1 ? 1 : (g > cap ? cap : g));
 }
 
@@ -113,7 +112,7 @@ int vec_bytes(int row_bytes) {
 
 }  // namespace
 
-cudaError_t launch_uly_pack_to(const void* x, const PeerDst& dst, int B, int L, int Lmax, int H, int D, int u,
+cudaError_t launch_uly_pack_to(const void* x, const ChunkDst& dst, int B, int L, int Lmax, int H, int D, int u,
                                int slot, int nslots, int elem_bytes, cudaStream_t st) {
   const int rb = D * elem_bytes, vb = vec_bytes(rb), vpr = rb / vb, Hh = H / u;
   const int64_t n = int64_t(B) * L * H * vpr;
@@ -132,7 +131,7 @@ cudaError_t launch_uly_pack_to(const void* x, const PeerDst& dst, int B, int L, 
 cudaError_t launch_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u,
                             int slot, int nslots, int elem_bytes, cudaStream_t st) {
   // send[p][slot][B][Lmax][H/u][D]: chunk p starts at p * nslots * (B * Lmax * H/u * D) elements
-  PeerDst dst{};
+  ChunkDst dst{};
   const size_t chunk_bytes = size_t(nslots) * B * Lmax * (H / u) * D * elem_bytes;
   for (int p = 0; p < u && p < 8; ++p) dst.p[p] = static_cast<char*>(send) + p * chunk_bytes;
   return launch_uly_pack_to(x, dst, B, L, Lmax, H, D, u, slot, nslots, elem_bytes, st);

@@ -185,11 +185,11 @@ cudaError_t launch_tc(const CUtensorMap& mx, const void* wt, const CUtensorMap& 
   CUtensorMap mw;
   if (!make_map(&mw, wt, 1, Co, 9, Ci, int64_t(9) * Co * Ci, Ci, int64_t(Co) * Ci, kKC, COT))
     return cudaErrorInvalidValue;
-  static bool attr = false;
-  if (!attr) {
+  static DeviceFlags attr;
+  if (!attr.test()) {
     cudaError_t e = cudaFuncSetAttribute(vae_conv_tc_kernel<COT>, cudaFuncAttributeMaxDynamicSharedMemorySize, T::kSmem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.set();
   }
   const dim3 grid((W + kPix - 1) / kPix, Hout, (Co + COT - 1) / COT);
   vae_conv_tc_kernel<COT><<<grid, 192, T::kSmem, st>>>(mx, mw, mo, b, Hout, W, Ci, Co, act_up);
@@ -210,11 +210,9 @@ cudaError_t launch_vae_conv_tc(const void* in, int Hout, int Ci, int W, const vo
                 int64_t(act_up ? 4 : 1) * Hout * W * Co8, Co8, int64_t(act_up ? 2 * W : W) * Co8, 32,
                 act_up ? 2 * kPix : kPix))
     return cudaErrorInvalidValue;
-  static const int cot = [] {  // XDIT_VAE_COT=128|256 overrides the choice (A/B)
-    const char* e = std::getenv("XDIT_VAE_COT");
-    return e ? std::atoi(e) : 0;
-  }();
-  const bool wide = cot ? cot == 256 : Co >= 256;
+  // 256 output channels per CTA for the wide layers (half the A-tile loads per FLOP), else 128
+  // (profiles/r01_ab_vae_cot.txt)
+  const bool wide = Co >= 256;
   return wide ? launch_tc<256>(mx, wt, mo, b, Hout, Ci, W, Co, act_up, st)
               : launch_tc<128>(mx, wt, mo, b, Hout, Ci, W, Co, act_up, st);
 }

@@ -12,6 +12,27 @@ namespace xdit {
 // Count one kernel launch of this library (xdit_launch_count()).
 void note_launches(int n);
 
+// SM count of the CURRENT device (cached per device ordinal: a process may drive several GPUs).
+int device_sm_count();
+
+// One flag per device ordinal (e.g. "cudaFuncSetAttribute done for this kernel on device d").
+struct DeviceFlags {
+  unsigned long long bits[2] = {0, 0};  // devices 0..127
+  static int cur() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & 127;
+  }
+  bool test() const {
+    const int d = cur();
+    return (__atomic_load_n(&bits[d >> 6], __ATOMIC_ACQUIRE) >> (d & 63)) & 1ull;
+  }
+  void set() {
+    const int d = cur();
+    __atomic_fetch_or(&bits[d >> 6], 1ull << (d & 63), __ATOMIC_RELEASE);
+  }
+};
+
 // Arguments of one attention launch (one Q block against one KV block).  Strides in elements.
 struct AttnArgs {
   const void* q;
@@ -34,7 +55,7 @@ struct AttnArgs {
   float* acc_l_out = nullptr;
   xdit_rowmap acc_map{};
 };
-// True when launch_attn_fwd_sm100 would run a kernel that implements the fused ring merge.
+// True when launch_attn_fwd_bf16 runs a kernel that implements the fused ring merge.
 bool attn_fused_merge_supported(int D);
 
 // fp32 scratch the bf16 attention kernel can use to split the last partial wave of its grid:
@@ -42,19 +63,18 @@ bool attn_fused_merge_supported(int D);
 size_t attn_scratch_floats(int D);
 
 // Launchers return cudaError_t (cudaSuccess on success); argument checks happen in xdit_usp.cpp.
-cudaError_t launch_attn_fwd_sm100(const AttnArgs& a, cudaStream_t st);  // bf16, D in {64,72,128}
-// CTA-pair (cta_group::2) variant of the bf16 kernel, used by launch_attn_fwd_sm100 where supported.
-bool attn_fwd_2sm_supports(int D);
-cudaError_t launch_attn_fwd_2sm(const AttnArgs& a, cudaStream_t st);
+// bf16, D in {64,72,128}: the CTA-pair (cta_group::2) tcgen05 kernel (attn_fwd_2sm.cu)
+cudaError_t launch_attn_fwd_bf16(const AttnArgs& a, cudaStream_t st);
 cudaError_t launch_attn_fwd_f32(const AttnArgs& a, cudaStream_t st);    // fp32 SIMT, D <= 256
 cudaError_t launch_lse_merge(float* o_acc, float* lse_acc, const float* o_s, const float* lse_s,
                              int B, int S, int Hh, int D, void* fin, float* fin_lse,
                              const xdit_rowmap* fmap, int fin_dtype, cudaStream_t st);
-// Per-Ulysses-peer destination base addresses of a pack (device pointers, local or peer-mapped).
-struct PeerDst {
+// Per-Ulysses-peer destination base addresses of a pack (the send chunk of each peer; this rank's
+// own head block goes straight to its receive chunk).
+struct ChunkDst {
   char* p[8];
 };
-cudaError_t launch_uly_pack_to(const void* x, const PeerDst& dst, int B, int L, int Lmax, int H, int D, int u,
+cudaError_t launch_uly_pack_to(const void* x, const ChunkDst& dst, int B, int L, int Lmax, int H, int D, int u,
                                int slot, int nslots, int elem_bytes, cudaStream_t st);
 cudaError_t launch_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u,
                             int slot, int nslots, int elem_bytes, cudaStream_t st);
@@ -67,6 +87,14 @@ cudaError_t launch_uly_unpack_out(const void* orecv, const float* lrecv, int64_t
                                   cudaStream_t st);
 
 // SURVEY §8(f) NEXT rows (next_ops.cu).
+// Where the rows of a K/V block land in a KV buffer: block rows [src[k], src[k+1]) (src[n] = the
+// block's row count) go to buffer rows dst[k] + (t - src[k]).
+struct KvSegs {
+  int n;
+  int src[16], dst[16];
+};
+cudaError_t launch_kv_place(const void* k, const void* v, void* kv, int B, int Hh, int S_blk, int S_total,
+                            const KvSegs& segs, int D, int64_t sb, int64_t ss, int64_t sh, int eb, cudaStream_t st);
 cudaError_t launch_kv_retain(const void* k, const void* v, void* kv_keep, int B, int Hh, int S_blk, int S_total,
                              int seq_off, int D, int64_t sb, int64_t ss, int64_t sh, int eb, cudaStream_t st);
 cudaError_t launch_cfg_combine(const void* c, const void* u, void* o, int64_t n, float g, int dtype,
@@ -77,6 +105,10 @@ size_t pf_workspace_bytes(int B, int n, int H, int D, int dtype);
 cudaError_t launch_pf_block(void* h, void* kv, const float* w, void* work, int B, int H, int S, int off, int n,
                             int D, int dtype, cudaStream_t st);
 cudaError_t launch_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype, cudaStream_t st);
+cudaError_t launch_pf_qkv(const void* h, const float* w, void* q, void* k, void* v, int B, int n, int H, int D,
+                          int dtype, cudaStream_t st);
+cudaError_t launch_pf_residual(void* h, const void* o, const float* w, int B, int n, int H, int D, int dtype,
+                               cudaStream_t st);
 
 // SURVEY §8(f) NEXT 4, patch-parallel VAE decode (vae.cu).
 cudaError_t launch_vae_conv3x3(const float* in, int Hout, int Ci, int W, const float* w, const float* b, float* out,
@@ -98,8 +130,8 @@ __host__ __device__ inline RowDst rowmap_dst(const xdit_rowmap& m, int b, int ro
     if (i < m.nseg && row >= m.seg_off[i]) s = i;
   const int64_t r = row - m.seg_off[s];
   RowDst d;
-  d.o_off = (m.seg_table ? m.o_seg_off[s] : s * m.o_seg) + b * m.o_b + r * m.o_s + h * m.o_h;
-  d.l_off = (m.seg_table ? m.l_seg_off[s] : s * m.l_seg) + b * m.l_b + h * m.l_h + r;
+  d.o_off = s * m.o_seg + b * m.o_b + r * m.o_s + h * m.o_h;
+  d.l_off = s * m.l_seg + b * m.l_b + h * m.l_h + r;
   return d;
 }
 

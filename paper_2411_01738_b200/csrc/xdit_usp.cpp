@@ -3,24 +3,15 @@
 // attention call (include/xdit_usp.h).
 //
 // USP (§4.1.4) on a 2D mesh, rank g = i*u + j (reading C6):
-//   Ulysses a2a within the row {i*u + j'} (§4.1.1), Ring P2P within the column {i'*u + j}
-//   (§4.1.1), every collective on an internal high-priority side stream joined back to the
-//   caller's stream with events; no host synchronisation anywhere in the call.
-//
-// Two transports move the bytes:
-//   * NCCL: grouped ncclSend/ncclRecv on the Ulysses / Ring sub-communicators;
-//   * peer memory (xdit_comm_init_peer): every rank maps the receive buffers of the ranks it sends
-//     to (CUDA IPC; over NVLink/NVSwitch between GPUs), the Ulysses pack kernel stores straight
-//     into the peers' receive buffers, ring KV blocks and O chunks are copied peer-to-peer, and the
-//     ranks order their streams with 32-bit flags in device memory -- cuStreamWriteValue32 into the
-//     peer's flag (preceded by a system-wide fence) and cuStreamWaitValue32 (>=) on the local one.
-//     No SM spins and no host thread waits, so the call stays stream-ordered and graph-capturable,
-//     and several ranks may even share one GPU (how the multi-rank tests run on a 1-GPU box).
-#include <cuda.h>
-#include <cudaTypedefs.h>
+//   Ulysses all-to-all within the row {i*u + j'} (§4.1.1) as grouped ncclSend/ncclRecv on the
+//   Ulysses sub-communicator, on the caller's stream (not overlapped); Ring P2P within the
+//   column {i'*u + j} (§4.1.1) as grouped ncclSend/ncclRecv on the Ring sub-communicator, on
+//   an internal high-priority side stream that runs while the attention kernel of the current ring
+//   step runs on the caller's stream (overlapped), joined back with events.  NCCL is the one
+//   data plane; no host synchronisation anywhere in the call, which stays CUDA-graph
+//   capturable.
 #include <cuda_runtime.h>
 #include <nccl.h>
-#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -37,6 +28,18 @@ using xdit::AttnArgs;
 namespace xdit {
 static std::atomic<unsigned long long> g_launches{0};
 void note_launches(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
+int device_sm_count() {
+  static std::atomic<int> cache[128];  // 0 = not queried yet
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 127;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n == 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 }  // namespace xdit
 
 namespace {
@@ -197,72 +200,37 @@ int check_map_align(const xdit_rowmap* m, int vec_elems) {
   for (int64_t x : v)
     if (x % vec_elems != 0)
       return fail(XDIT_ERR_ALIGNMENT, "output strides must be multiples of %d elements", vec_elems);
-  if (m->seg_table)
-    for (int s = 0; s < m->nseg && s < 8; ++s)
-      if (m->o_seg_off[s] % vec_elems != 0)
-        return fail(XDIT_ERR_ALIGNMENT, "segment offsets must be multiples of %d elements", vec_elems);
   return XDIT_OK;
 }
 
 }  // namespace
 
 namespace {
-// Peer-memory transport: exported buffers (blob handle index) and flag words.
-enum { kHUly = 0, kHORecv = 1, kHKV = 2 /* kHKV + 2*slot + (0 K, 1 V) */, kHFlags = 6, kHMbox = 7, kNHandles = 8 };
-// flag words: Ulysses data, O return, ring data / credit, mailbox data / ack (per source rank),
-// CFG tail data / ack
-enum { kFA2A = 0, kFO = 8, kFData = 16, kFCredit = 18, kFP2P = 32, kFAck = 40, kFCfg = 48, kFCfgAck = 50,
-       kFlagWords = 64 };
-constexpr uint32_t kBlobMagic = 0x31504458u;  // "XDP1"
-struct PeerBlob {
-  uint32_t magic;
-  int32_t rank, nranks, u, r, device, pid;
-  uint32_t valid;                    // bit k: handle k exported
-  uint64_t bytes[kNHandles];         // allocation sizes
-  cudaIpcMemHandle_t h[kNHandles];
-};
-static_assert(sizeof(PeerBlob) <= XDIT_PEER_BLOB_BYTES, "peer blob size");
 
-struct MemOps {
-  PFN_cuStreamWaitValue32_v11070 wait = nullptr;
-  PFN_cuStreamWriteValue32_v11070 write = nullptr;
+// CTAs NCCL may use for the ring's send/recv: they run while the attention grid holds every SM, so
+// the ring only borrows the SMs its transfer needs -- Flux 1x8 moves 89 MB per step in ~0.84 ms of
+// attention, 106 GB/s, a few channels of NVLink 5.  The Ulysses exchange is not
+// overlapped and keeps NCCL's default (all channels).
+constexpr int kRingMaxCTAs = 16;
+
+struct Prof {  // per-phase timing events of the last call (xdit_comm_profile)
+  bool on = false, made = false, recorded = false;
+  cudaEvent_t t0 = nullptr, t_a2a = nullptr, t_end = nullptr, t_step[8] = {}, c0[8] = {}, c1[8] = {};
+  xdit_phases ph{};
 };
-const MemOps* memops() {
-  static MemOps m = [] {
-    MemOps x;
-    cudaDriverEntryPointQueryResult q;
-    void* f = nullptr;
-    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      x.wait = reinterpret_cast<PFN_cuStreamWaitValue32_v11070>(f);
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
-        q == cudaDriverEntryPointSuccess)
-      x.write = reinterpret_cast<PFN_cuStreamWriteValue32_v11070>(f);
-    return x;
-  }();
-  return (m.wait && m.write) ? &m : nullptr;
-}
-struct PeerMap {
-  void* ptr[kNHandles] = {};
-  uint64_t bytes[kNHandles] = {};
-  bool opened[kNHandles] = {};  // true: an IPC mapping this handle must close
-};
+
 }  // namespace
 
 struct xdit_comm_s {
   int nranks = 1, rank = 0, u = 1, r = 1, device = 0;
-  int transport = XDIT_TRANSPORT_NCCL;
-  uint32_t* flags = nullptr;  // peer transport: kFlagWords words written by the peers
-  bool connected = false;
-  std::vector<PeerMap> peer;  // peer transport: per SP rank (self = local pointers)
-  size_t mbox_region = 0;     // peer transport: mailbox bytes per source rank
-  uint32_t cfg_epoch = 0;     // peer transport: xdit_cfg_tail calls issued
-  ncclComm_t sp = nullptr, uly = nullptr, ring = nullptr;
+  ncclComm_t sp = nullptr;    // the SP group's communicator (the caller's, or ours: own_sp)
+  ncclComm_t all = nullptr;   // private communicator over the whole group (p2p, all-gather)
+  ncclComm_t uly = nullptr, ring = nullptr;  // Ulysses row / Ring column
   bool own_sp = false;
   cudaStream_t side = nullptr;
-  cudaEvent_t ev_start = nullptr, ev_a2a = nullptr, ev_o = nullptr, ev_o_a2a = nullptr;
-  cudaEvent_t ev_kdone[2] = {nullptr, nullptr}, ev_recv[2] = {nullptr, nullptr};
-  Buf uly_send, uly_recv, qblk, kv[2][2], oacc, lacc, otmp, ltmp, osend, orecv, tail, mbox;
+  cudaEvent_t ev_fork = nullptr, ev_recv[2] = {nullptr, nullptr};
+  Buf uly_send, uly_recv, qblk, kv[2][2], oacc, lacc, otmp, ltmp, osend, orecv, tail;
+  Prof prof;
 };
 
 namespace {
@@ -272,27 +240,32 @@ int comm_finish_init(xdit_comm_s* c) {
   int lo = 0, hi = 0;
   XCUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   XCUDA(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, hi));
-  cudaEvent_t* evs[] = {&c->ev_start, &c->ev_a2a, &c->ev_o, &c->ev_o_a2a,
-                        &c->ev_kdone[0], &c->ev_kdone[1], &c->ev_recv[0], &c->ev_recv[1]};
+  cudaEvent_t* evs[] = {&c->ev_fork, &c->ev_recv[0], &c->ev_recv[1]};
   for (cudaEvent_t* e : evs) XCUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
-  if (c->transport == XDIT_TRANSPORT_PEER) {
-    if (!memops()) return fail(XDIT_ERR_UNSUPPORTED, "stream memory operations (cuStreamWaitValue32) unavailable");
-    XCUDA(cudaMalloc(&c->flags, kFlagWords * sizeof(uint32_t)));
-    XCUDA(cudaMemset(c->flags, 0, kFlagWords * sizeof(uint32_t)));
-    const uint32_t one = 1;  // my ring successor's slot 1 is free before the first call
-    XCUDA(cudaMemcpy(c->flags + kFCredit + 1, &one, sizeof one, cudaMemcpyHostToDevice));
-    XCUDA(cudaDeviceSynchronize());  // zeroed before any peer can map and write them
-  } else if (c->nranks > 1) {
+  if (c->nranks > 1) {
     const int i = c->rank / c->u, j = c->rank % c->u;
     // ncclCommSplit is collective over the SP communicator; every rank takes the same branches.
-    if (c->u > 1) XNCCL(ncclCommSplit(c->sp, i, j, &c->uly, nullptr));
-    if (c->r > 1) XNCCL(ncclCommSplit(c->sp, j, i, &c->ring, nullptr));
+    if (c->own_sp) {
+      c->all = c->sp;
+    } else {  // never issue work on the caller's communicator: a private copy for p2p / all-gather
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      XNCCL(ncclCommSplit(c->sp, 0, c->rank, &c->all, &cfg));
+    }
+    if (c->u > 1) {
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      XNCCL(ncclCommSplit(c->sp, i, j, &c->uly, &cfg));
+    }
+    if (c->r > 1) {
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.maxCTAs = kRingMaxCTAs;
+      XNCCL(ncclCommSplit(c->sp, j, i, &c->ring, &cfg));
+    }
   }
   return XDIT_OK;
 }
 
 int check_async(xdit_comm_s* c) {
-  ncclComm_t cs[3] = {c->sp, c->uly, c->ring};
+  ncclComm_t cs[3] = {c->all, c->uly, c->ring};
   for (ncclComm_t x : cs) {
     if (!x) continue;
     ncclResult_t st = ncclSuccess;
@@ -303,62 +276,13 @@ int check_async(xdit_comm_s* c) {
   return XDIT_OK;
 }
 
-// ---- peer-memory transport helpers
-void close_peers(xdit_comm_s* c) {
-  for (PeerMap& m : c->peer)
-    for (int k = 0; k < kNHandles; ++k)
-      if (m.opened[k] && m.ptr[k]) cudaIpcCloseMemHandle(m.ptr[k]);
-  c->peer.clear();
-  c->connected = false;
-}
-
-// Local exported buffers by handle index.
-Buf* exported(xdit_comm_s* c, int k) {
-  switch (k) {
-    case kHUly: return &c->uly_recv;
-    case kHORecv: return &c->orecv;
-    case kHKV + 0: return &c->kv[0][0];
-    case kHKV + 1: return &c->kv[0][1];
-    case kHKV + 2: return &c->kv[1][0];
-    case kHKV + 3: return &c->kv[1][1];
-    case kHMbox: return &c->mbox;
-    default: return nullptr;
-  }
-}
-
-// Stream-ordered signal: *peer_flag = v after all prior work of `st` (system-wide fence first).
-int post_flag(cudaStream_t st, uint32_t* peer_flag, uint32_t v) {
-  const CUresult r = memops()->write(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(peer_flag), v,
-                                     CU_STREAM_WRITE_VALUE_DEFAULT);
-  if (r != CUDA_SUCCESS) return fail(XDIT_ERR_CUDA, "cuStreamWriteValue32 failed (%d)", int(r));
-  return XDIT_OK;
-}
-// Stream-ordered wait: later work of `st` starts once (int32)(*flag - v) >= 0.
-int wait_flag(cudaStream_t st, const uint32_t* flag, uint32_t v) {
-  const CUresult r = memops()->wait(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(flag), v,
-                                    CU_STREAM_WAIT_VALUE_GEQ);
-  if (r != CUDA_SUCCESS) return fail(XDIT_ERR_CUDA, "cuStreamWaitValue32 failed (%d)", int(r));
-  return XDIT_OK;
-}
-
-// Byte-exact all-to-all of `chunk` bytes per peer on `comm` (send[p] -> peer p -> recv[p]).
-int a2a(ncclComm_t comm, int n, const void* send, void* recv, size_t chunk, cudaStream_t st) {
-  XNCCL(ncclGroupStart());
-  for (int p = 0; p < n; ++p) {
-    XNCCL(ncclSend(static_cast<const char*>(send) + p * chunk, chunk, ncclUint8, p, comm, st));
-    XNCCL(ncclRecv(static_cast<char*>(recv) + p * chunk, chunk, ncclUint8, p, comm, st));
-  }
-  XNCCL(ncclGroupEnd());
-  return XDIT_OK;
-}
-
 int attn_launch(const AttnArgs& a_in, int dtype, cudaStream_t st, const Buf* scratch = nullptr) {
   AttnArgs a = a_in;
   if (scratch && scratch->p) {
     a.scratch = static_cast<float*>(scratch->p);
     a.scratch_floats = scratch->bytes / sizeof(float);
   }
-  cudaError_t e = dtype == 0 ? xdit::launch_attn_fwd_sm100(a, st) : xdit::launch_attn_fwd_f32(a, st);
+  cudaError_t e = dtype == 0 ? xdit::launch_attn_fwd_bf16(a, st) : xdit::launch_attn_fwd_f32(a, st);
   if (e != cudaSuccess)
     return fail(XDIT_ERR_CUDA, "attention launch failed: %s", cudaGetErrorString(e));
   return XDIT_OK;
@@ -370,10 +294,29 @@ int attn_launch(const AttnArgs& a_in, int dtype, cudaStream_t st, const Buf* scr
     if (rc_ != XDIT_OK) return rc_; \
   } while (0)
 
+// Timing event of phase `e` on stream `s`, only while profiling and outside a graph capture.
+struct Marks {
+  Prof* p;
+  bool on;
+  int rec(cudaEvent_t e, cudaStream_t s) {
+    if (on) XCUDA(cudaEventRecord(e, s));
+    return XDIT_OK;
+  }
+};
+
+// What a call does with the K,V it holds besides attending to them (NEXT 1 / NEXT 3).
+struct KvOpts {
+  void* keep = nullptr;  // xdit_usp_attention_kv: retain the SP group's K,V (reading R2)
+  void* buf = nullptr;   // xdit_usp_attention_buf: write the fresh K,V into the persistent buffer at
+  int S_buf = 0;         //   the tokens' rows (text token t -> txt_row + t, image token t -> img_row + t)
+  int txt_row = 0;       //   and attend over all of it (reading R6)
+  int img_row = 0;
+};
+
 // One USP attention call; eb = element bytes (2: bf16 / tcgen05 path, 4: fp32 / SIMT path).
 int usp_call(const void* q, const void* k, const void* v, void* out, float* lse, int B, int H,
              int S_txt, int S_img, int D, int u, int r, cudaStream_t st, xdit_comm_s* c, int eb,
-             void* kv_keep = nullptr) {
+             const KvOpts& kvo = KvOpts{}) {
   if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
   if (!q || !k || !v || !out) return fail(XDIT_ERR_INVALID_ARG, "q/k/v/out must not be NULL");
   if (u != c->u || r != c->r || u * r != c->nranks)
@@ -384,53 +327,75 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     return fail(XDIT_ERR_UNSUPPORTED, "bf16 path supports D in {64,72,128}, got %d", D);
   if (dtype == 1 && (D < 1 || D > 256))
     return fail(XDIT_ERR_UNSUPPORTED, "fp32 path supports D in [1,256], got %d", D);
-  if (dtype == 1 && u * r > 1 && (D % 4) != 0)
-    return fail(XDIT_ERR_UNSUPPORTED, "fp32 multi-rank path needs D %% 4 == 0, got %d", D);
+  if (dtype == 1 && (u * r > 1 || kvo.keep || kvo.buf) && (D % 4) != 0)
+    return fail(XDIT_ERR_UNSUPPORTED, "fp32 multi-rank / KV-buffer path needs D %% 4 == 0, got %d", D);
   if (!aligned16(q) || !aligned16(k) || !aligned16(v) || !aligned16(out) || !aligned16(lse) ||
-      !aligned16(kv_keep))
+      !aligned16(kvo.keep) || !aligned16(kvo.buf))
     return fail(XDIT_ERR_ALIGNMENT, "tensor pointers must be 16-byte aligned");
   if ((int64_t(H) * D * eb) % 16 != 0)
     return fail(XDIT_ERR_ALIGNMENT, "H*D*elem_bytes must be a multiple of 16");
   Plan P;
   XRET(make_plan(B, H, S_txt, S_img, D, u, r, c->rank, &P));
+  const int S_sp = S_txt + S_img;
+  if (kvo.buf && (kvo.txt_row < 0 || kvo.img_row < 0 || kvo.txt_row + S_txt > kvo.S_buf ||
+                  kvo.img_row + S_img > kvo.S_buf))
+    return fail(XDIT_ERR_INVALID_ARG, "KV buffer rows (text at %d, image at %d) exceed S_buf=%d", kvo.txt_row,
+                kvo.img_row, kvo.S_buf);
   const Sizes need = sizes_for(P, B, D, eb);
   if (need.uly3 > c->uly_recv.bytes || need.qblk > c->qblk.bytes || need.kvslot > c->kv[1][0].bytes ||
       need.oacc > c->oacc.bytes || need.lacc > c->lacc.bytes || need.ochunk * P.u > c->osend.bytes * (P.u > 1))
     return fail(XDIT_ERR_WORKSPACE, "problem exceeds the reservation; call xdit_comm_reserve first");
   XRET(check_async(c));
-  const bool peer = c->transport == XDIT_TRANSPORT_PEER && P.N > 1;
-  if (peer) {
-    if (!c->connected)
-      return fail(XDIT_ERR_NOT_CONNECTED, "peer transport: call xdit_comm_peer_connect after xdit_comm_reserve");
-    for (int q = 0; q < P.N; ++q) {  // buffers this rank writes into on peer q
-      const PeerMap& m = c->peer[q];
-      const bool uly_peer = q / P.u == P.i && P.u > 1, ring_next = q == ((P.i + 1) % P.r) * P.u + P.j && P.r > 1;
-      bool ok = !(uly_peer || ring_next) || m.ptr[kHFlags];
-      if (uly_peer) ok = ok && m.bytes[kHUly] >= need.uly3 && m.bytes[kHORecv] >= need.ochunk * P.u;
-      if (ring_next)
-        for (int k = 0; k < 4; ++k) ok = ok && m.bytes[kHKV + k] >= need.kvslot;
-      if (!ok)
-        return fail(XDIT_ERR_WORKSPACE,
-                    "peer %d's mapped workspace is smaller than this problem (flags %p, uly %llu/%zu, orecv %llu/%zu, "
-                    "kv %llu/%zu)", q, m.ptr[kHFlags], (unsigned long long)m.bytes[kHUly], need.uly3,
-                    (unsigned long long)m.bytes[kHORecv], need.ochunk * P.u, (unsigned long long)m.bytes[kHKV],
-                    need.kvslot);
-    }
-  }
-  // Peer transport flags are binary: the writer sets 1 (after its data), the owner waits for 1 and
-  // resets 0 before anything that lets the writer set it again -- so every stream operation carries
-  // constant values and the call replays correctly from a captured CUDA graph.
+
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  XCUDA(cudaStreamIsCapturing(st, &cap));
+  Prof& pf = c->prof;
+  Marks mk{&pf, pf.on && pf.made && cap == cudaStreamCaptureStatusNone};
+  pf.recorded = mk.on;
+  pf.ph = xdit_phases{};
+  pf.ph.ulysses = u;
+  pf.ph.ring = r;
 
   const int i = P.i, Hh = P.Hh, L = P.S_loc[c->rank], Sb = P.S_blk[i];
   const int64_t row = int64_t(Hh) * D;  // elements per (token) row of a head-block tensor
-  // NEXT 1 (reading R2): the KV buffer holds every ring block at its offset in SP-shard order
-  const int S_sp = S_txt + S_img;
-  auto blk_off = [&](int ib) {
+  auto blk_off = [&](int ib) {  // sequence offset of ring block ib in SP-shard order (R2 / R6)
     int o = 0;
     for (int x = 0; x < ib; ++x) o += P.S_blk[x];
     return o;
   };
+  void* kvdst = kvo.keep ? kvo.keep : kvo.buf;       // where held K,V blocks are copied to
+  const int kv_total = kvo.keep ? S_sp : kvo.S_buf;  // its sequence length
+  // rows of ring block ib in it: kv_keep in SP-shard order (R2), kv_buf at the tokens' own rows (R6)
+  auto segs_of = [&](int ib) {
+    xdit::KvSegs sg{};
+    if (kvo.keep) {
+      sg.n = 1;
+      sg.dst[0] = blk_off(ib);
+      return sg;
+    }
+    int bo = 0;
+    for (int p = 0; p < P.u; ++p) {
+      int to, tl, io, il;
+      piece(S_txt, P.N, ib * P.u + p, &to, &tl);
+      piece(S_img, P.N, ib * P.u + p, &io, &il);
+      if (tl) sg.src[sg.n] = bo, sg.dst[sg.n++] = kvo.txt_row + to;
+      if (il) sg.src[sg.n] = bo + tl, sg.dst[sg.n++] = kvo.img_row + io;
+      bo += tl + il;
+    }
+    return sg;
+  };
+  // the attention over the whole KV buffer (xdit_usp_attention_buf): Q block x kv_buf
+  auto buf_attention = [&](AttnArgs a) {
+    a.k = kvo.buf;
+    a.v = static_cast<const char*>(kvo.buf) + size_t(B) * Hh * kvo.S_buf * D * eb;
+    a.Skv = kvo.S_buf;
+    a.kv_b = int64_t(Hh) * kvo.S_buf * D;
+    a.kv_s = D;
+    a.kv_h = int64_t(kvo.S_buf) * D;
+    return attn_launch(a, dtype, st, &c->tail);
+  };
 
+  XRET(mk.rec(pf.t0, st));
   // ---- N == 1: one kernel straight from the caller's tensors into the caller's output
   if (P.N == 1) {
     AttnArgs a{};
@@ -439,43 +404,36 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     a.q_b = a.kv_b = int64_t(L) * H * D; a.q_s = a.kv_s = int64_t(H) * D; a.q_h = a.kv_h = D;
     a.omap = plain_map(B, L, H, D);
     a.out_f32 = dtype;
-    if (kv_keep)
-      XCUDA(xdit::launch_kv_retain(k, v, kv_keep, B, H, L, S_sp, 0, D, a.kv_b, a.kv_s, a.kv_h, eb, st));
-    return attn_launch(a, dtype, st, &c->tail);
+    if (kvdst)
+      XCUDA(xdit::launch_kv_place(k, v, kvdst, B, H, L, kv_total, segs_of(0), D, a.kv_b, a.kv_s, a.kv_h, eb, st));
+    XRET(mk.rec(pf.t_a2a, st));
+    XRET(kvo.buf ? buf_attention(a) : attn_launch(a, dtype, st, &c->tail));
+    XRET(mk.rec(pf.t_step[0], st));
+    XRET(mk.rec(pf.t_end, st));
+    return XDIT_OK;
   }
 
-  XCUDA(cudaEventRecord(c->ev_start, st));
-  XCUDA(cudaStreamWaitEvent(c->side, c->ev_start, 0));
-
-  // ---- a2-a4: Ulysses all-to-all of Q, K, V (scatter heads, gather sequence)
+  // ---- a2-a4: Ulysses all-to-all of Q, K, V (scatter heads, gather sequence), caller's stream
   const void *Qp = q, *Kc = k, *Vc = v;
   int64_t q_b = int64_t(L) * H * D, q_s = int64_t(H) * D;
   if (P.u > 1) {
     const void* src[3] = {q, k, v};
-    if (peer) {
-      // pack = all-to-all: head block p of every local token is stored straight into Ulysses peer
-      // p's receive buffer at this rank's chunk (P.j); then flag each peer and wait for theirs.
-      xdit::PeerDst pd{};
-      for (int p = 0; p < P.u; ++p)
-        pd.p[p] = static_cast<char*>(c->peer[i * P.u + p].ptr[kHUly]) + size_t(P.j) * (need.uly3 / P.u);
-      for (int t = 0; t < 3; ++t)
-        XCUDA(xdit::launch_uly_pack_to(src[t], pd, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
-      for (int p = 0; p < P.u; ++p)
-        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFA2A + P.j, 1));
-      for (int p = 0; p < P.u; ++p)
-        if (p != P.j) {  // peer p sets it again only after my O return of this call (after this reset)
-          XRET(wait_flag(st, c->flags + kFA2A + p, 1));
-          XRET(post_flag(st, c->flags + kFA2A + p, 0));
-        }
-    } else {
-      for (int t = 0; t < 3; ++t)
-        XCUDA(xdit::launch_uly_pack(src[t], c->uly_send.p, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
-      XCUDA(cudaEventRecord(c->ev_a2a, st));
-      XCUDA(cudaStreamWaitEvent(c->side, c->ev_a2a, 0));
-      XRET(a2a(c->uly, P.u, c->uly_send.p, c->uly_recv.p, need.uly3 / P.u, c->side));
-      XCUDA(cudaEventRecord(c->ev_a2a, c->side));
-      XCUDA(cudaStreamWaitEvent(st, c->ev_a2a, 0));
+    const size_t chunk = need.uly3 / P.u;  // [3][B][Lmax][Hh][D] per peer
+    // pack: head block p of every local token into peer p's send chunk; this rank's own head
+    // block (p = j) straight into its receive chunk (no self-message)
+    xdit::ChunkDst cd{};
+    for (int p = 0; p < P.u; ++p)
+      cd.p[p] = static_cast<char*>(p == P.j ? c->uly_recv.p : c->uly_send.p) + size_t(p) * chunk;
+    for (int t = 0; t < 3; ++t)
+      XCUDA(xdit::launch_uly_pack_to(src[t], cd, B, L, P.Lmax, H, D, P.u, t, 3, eb, st));
+    XNCCL(ncclGroupStart());
+    for (int p = 0; p < P.u; ++p) {
+      if (p == P.j) continue;
+      XNCCL(ncclSend(static_cast<const char*>(c->uly_send.p) + p * chunk, chunk, ncclUint8, p, c->uly, st));
+      XNCCL(ncclRecv(static_cast<char*>(c->uly_recv.p) + p * chunk, chunk, ncclUint8, p, c->uly, st));
     }
+    XNCCL(ncclGroupEnd());
+    pf.ph.a2a_in_bytes = int64_t(P.u - 1) * int64_t(chunk);
     int len[8] = {0};
     for (int p = 0; p < P.u; ++p) len[p] = P.S_loc[i * P.u + p];
     XCUDA(xdit::launch_uly_unpack(c->uly_recv.p, c->qblk.p, B, P.Lmax, Hh, D, P.u, len, 0, 3, eb, st));
@@ -487,11 +445,13 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     q_b = int64_t(Sb) * row;
     q_s = row;
   }
-  if (kv_keep)  // this rank's ring block, right after the all-to-all (or straight from the caller)
-    XCUDA(xdit::launch_kv_retain(Kc, Vc, kv_keep, B, Hh, Sb, S_sp, blk_off(i), D, q_b, q_s, D, eb, st));
+  if (kvdst)  // this rank's ring block, right after the all-to-all (or straight from the caller)
+    XCUDA(xdit::launch_kv_place(Kc, Vc, kvdst, B, Hh, Sb, kv_total, segs_of(i), D, q_b, q_s, D, eb, st));
+  XRET(mk.rec(pf.t_a2a, st));
 
   // ---- destination of the final O / LSE: the caller's tensors (u == 1) or the reverse-a2a
-  //      send buffer, one segment per Ulysses peer (u > 1; reading C15)
+  //      send buffer, one segment per Ulysses peer (u > 1; reading C15) -- a8 fused into the
+  //      epilogue that writes the final result
   void* dst = out;
   float* dst_lse = lse;
   xdit_rowmap fmap = plain_map(B, L, H, D);
@@ -509,17 +469,6 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     fmap.l_seg = int64_t(need.ochunk / 4);
     fmap.l_b = int64_t(Hh) * P.Lmax;
     fmap.l_h = P.Lmax;
-    if (peer) {  // a9 fused into the epilogue: segment p is stored straight into peer p's O receive
-                 // buffer at this rank's chunk (P.j); the final kernel's stores are the all-to-all
-      fmap.seg_table = 1;
-      const char* ob = static_cast<const char*>(dst);
-      const char* lb = reinterpret_cast<const char*>(dst_lse);
-      for (int p = 0; p < P.u; ++p) {
-        const char* chunk = static_cast<const char*>(c->peer[i * P.u + p].ptr[kHORecv]) + size_t(P.j) * need.ochunk;
-        fmap.o_seg_off[p] = (chunk - ob) / eb;
-        fmap.l_seg_off[p] = (chunk + need.ochunk_o - lb) / 4;
-      }
-    }
   }
 
   AttnArgs a{};
@@ -530,22 +479,13 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     a.k = Kc; a.v = Vc; a.Skv = Sb;
     a.kv_b = q_b; a.kv_s = q_s; a.kv_h = D;
     a.o = dst; a.lse = dst_lse; a.omap = fmap; a.out_f32 = dtype;
-    XRET(attn_launch(a, dtype, st, &c->tail));
+    XRET(kvo.buf ? buf_attention(a) : attn_launch(a, dtype, st, &c->tail));
+    XRET(mk.rec(pf.t_step[0], st));
   } else {
-    // ---- a5-a7: ring loop; step s attends to the KV block of ring index (i - s) mod r (C9)
-    const int nxt_peer = (i + 1) % P.r, prv_peer = (i - 1 + P.r) % P.r;
-    // peer transport: slot credits.  Rank i pushes its current block into next's slot (s+1)&1 at
-    // step s <= r-2 once next's credit for that slot is set (it waits, resets, pushes, sets next's
-    // data flag).  A rank posts credit[s&1] to prev exactly once per push prev will make into that
-    // slot: after step 0 (slot 0, pushed at prev's step 1, if r >= 3), after steps 1..r-3 (pushed at
-    // prev's step s+1), and after its last odd step (slot 1, pushed at prev's step 0 of the NEXT
-    // call; credit[1] starts set).  Each post follows the reader's last use of the slot and its own
-    // push out of it, and every wait is matched by one post, so the flags end each call in the
-    // state they started it (credit[1] = 1, the rest 0).
-    const PeerMap* pnext = peer ? &c->peer[nxt_peer * P.u + P.j] : nullptr;
-    const PeerMap* pprev = peer ? &c->peer[prv_peer * P.u + P.j] : nullptr;
-    const int last_odd = ((P.r - 1) & 1) ? P.r - 1 : P.r - 2;  // r >= 2
-    auto credit_after = [&](int st_) { return (st_ == 0 && P.r >= 3) || (st_ >= 1 && st_ <= P.r - 3) || st_ == last_odd; };
+    // ---- a5-a7: ring loop; step s attends to the KV block of ring index (i - s) mod r (C9) on the
+    //      caller's stream while the side stream sends that block to i+1 and receives block
+    //      (i - s - 1) mod r from i-1 into the other slot (Table 1: overlapped)
+    const int nxt = (i + 1) % P.r, prv = (i - 1 + P.r) % P.r;
     const void* curK = Kc;
     const void* curV = Vc;
     xdit_rowmap accmap = plain_map(B, Sb, Hh, D);
@@ -558,103 +498,123 @@ int usp_call(const void* q, const void* k, const void* v, void* out, float* lse,
     for (int s = 0; s < P.r; ++s) {
       const int src = ((i - s) % P.r + P.r) % P.r;
       const int Skv = P.S_blk[src];
+      const int nsrc = ((src - 1) % P.r + P.r) % P.r;
       const int nslot = (s + 1) & 1;
       if (s < P.r - 1) {
-        // side stream: current block must be complete (recorded on st), next slot must be free
-        XCUDA(cudaEventRecord(c->ev_start, st));
-        XCUDA(cudaStreamWaitEvent(c->side, c->ev_start, 0));
-        const int nsrc = ((src - 1) % P.r + P.r) % P.r;
+        // side stream: the current block is complete and the other slot is free (its last reader,
+        // step s-1's attention, precedes this point of the caller's stream)
+        XCUDA(cudaEventRecord(c->ev_fork, st));
+        XCUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+        XRET(mk.rec(pf.c0[s], c->side));
         const size_t sbytes = size_t(B) * Skv * row * eb, rbytes = size_t(B) * P.S_blk[nsrc] * row * eb;
-        if (peer) {
-          XRET(wait_flag(c->side, c->flags + kFCredit + nslot, 1));
-          XRET(post_flag(c->side, c->flags + kFCredit + nslot, 0));
-          XCUDA(cudaMemcpyAsync(pnext->ptr[kHKV + 2 * nslot], curK, sbytes, cudaMemcpyDefault, c->side));
-          XCUDA(cudaMemcpyAsync(pnext->ptr[kHKV + 2 * nslot + 1], curV, sbytes, cudaMemcpyDefault, c->side));
-          XRET(post_flag(c->side, static_cast<uint32_t*>(pnext->ptr[kHFlags]) + kFData + nslot, 1));
-          (void)rbytes;
-        } else {
-          XNCCL(ncclGroupStart());
-          XNCCL(ncclSend(curK, sbytes, ncclUint8, nxt_peer, c->ring, c->side));
-          XNCCL(ncclSend(curV, sbytes, ncclUint8, nxt_peer, c->ring, c->side));
-          XNCCL(ncclRecv(c->kv[nslot][0].p, rbytes, ncclUint8, prv_peer, c->ring, c->side));
-          XNCCL(ncclRecv(c->kv[nslot][1].p, rbytes, ncclUint8, prv_peer, c->ring, c->side));
-          XNCCL(ncclGroupEnd());
-        }
+        XNCCL(ncclGroupStart());
+        XNCCL(ncclSend(curK, sbytes, ncclUint8, nxt, c->ring, c->side));
+        XNCCL(ncclSend(curV, sbytes, ncclUint8, nxt, c->ring, c->side));
+        XNCCL(ncclRecv(c->kv[nslot][0].p, rbytes, ncclUint8, prv, c->ring, c->side));
+        XNCCL(ncclRecv(c->kv[nslot][1].p, rbytes, ncclUint8, prv, c->ring, c->side));
+        XNCCL(ncclGroupEnd());
+        pf.ph.ring_bytes[s] = int64_t(2 * sbytes);
+        XRET(mk.rec(pf.c1[s], c->side));
         XCUDA(cudaEventRecord(c->ev_recv[s & 1], c->side));
       }
-      a.k = curK; a.v = curV; a.Skv = Skv;
-      a.kv_b = int64_t(Skv) * row; a.kv_s = row; a.kv_h = D;
-      a.omap = accmap; a.out_f32 = 1;
-      a.merge = 0;
-      if (s == 0) {
-        a.o = c->oacc.p; a.lse = static_cast<float*>(c->lacc.p);
-      } else if (fuse) {
-        const bool last = s == P.r - 1;
-        a.merge = 1;
-        a.merge_final = last ? 1 : 0;
-        a.acc_o = static_cast<float*>(c->oacc.p);
-        a.acc_l_in = l_in;
-        a.acc_l_out = l_out;
-        a.acc_map = accmap;
-        if (last) {
-          a.o = dst; a.lse = dst_lse; a.omap = fmap; a.out_f32 = dtype;
+      if (!kvo.buf) {
+        a.k = curK; a.v = curV; a.Skv = Skv;
+        a.kv_b = int64_t(Skv) * row; a.kv_s = row; a.kv_h = D;
+        a.omap = accmap; a.out_f32 = 1;
+        a.merge = 0;
+        if (s == 0) {
+          a.o = c->oacc.p; a.lse = static_cast<float*>(c->lacc.p);
+        } else if (fuse) {
+          const bool last = s == P.r - 1;
+          a.merge = 1;
+          a.merge_final = last ? 1 : 0;
+          a.acc_o = static_cast<float*>(c->oacc.p);
+          a.acc_l_in = l_in;
+          a.acc_l_out = l_out;
+          a.acc_map = accmap;
+          if (last) {
+            a.o = dst; a.lse = dst_lse; a.omap = fmap; a.out_f32 = dtype;
+          }
+        } else {
+          a.o = c->otmp.p; a.lse = static_cast<float*>(c->ltmp.p);
         }
-      } else {
-        a.o = c->otmp.p; a.lse = static_cast<float*>(c->ltmp.p);
+        XRET(attn_launch(a, dtype, st, &c->tail));
+        if (fuse && s > 0) std::swap(l_in, l_out);
+        if (s > 0 && !fuse) {
+          const bool last = s == P.r - 1;
+          XCUDA(xdit::launch_lse_merge(static_cast<float*>(c->oacc.p), static_cast<float*>(c->lacc.p),
+                                       static_cast<const float*>(c->otmp.p),
+                                       static_cast<const float*>(c->ltmp.p), B, Sb, Hh, D,
+                                       last ? dst : nullptr, last ? dst_lse : nullptr, &fmap,
+                                       dtype == 0 ? 0 : 1, st));
+        }
       }
-      XRET(attn_launch(a, dtype, st, &c->tail));
-      if (fuse && s > 0) std::swap(l_in, l_out);
-      if (s > 0 && !fuse) {
-        const bool last = s == P.r - 1;
-        XCUDA(xdit::launch_lse_merge(static_cast<float*>(c->oacc.p), static_cast<float*>(c->lacc.p),
-                                     static_cast<const float*>(c->otmp.p),
-                                     static_cast<const float*>(c->ltmp.p), B, Sb, Hh, D,
-                                     last ? dst : nullptr, last ? dst_lse : nullptr, &fmap,
-                                     dtype == 0 ? 0 : 1, st));
-      }
+      XRET(mk.rec(pf.t_step[s], st));
       if (s < P.r - 1) {
-        XCUDA(cudaStreamWaitEvent(st, c->ev_recv[s & 1], 0));  // (peer: my push out of this block is done)
-        if (peer) {
-          if (credit_after(s)) XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), 1));
-          XRET(wait_flag(st, c->flags + kFData + nslot, 1));
-          XRET(post_flag(st, c->flags + kFData + nslot, 0));
-        }
+        XCUDA(cudaStreamWaitEvent(st, c->ev_recv[s & 1], 0));  // block (i-s-1) arrived, my send is done
         curK = c->kv[nslot][0].p;
         curV = c->kv[nslot][1].p;
-        if (kv_keep) {  // the incoming ring block (index (i - s - 1) mod r) joins the KV buffer
-          const int nsrc = ((src - 1) % P.r + P.r) % P.r;
-          XCUDA(xdit::launch_kv_retain(curK, curV, kv_keep, B, Hh, P.S_blk[nsrc], S_sp, blk_off(nsrc), D,
-                                       int64_t(P.S_blk[nsrc]) * row, row, D, eb, st));
-        }
-      } else if (peer && credit_after(s)) {  // last step odd: slot 1's credit for prev's next call
-        XRET(post_flag(st, static_cast<uint32_t*>(pprev->ptr[kHFlags]) + kFCredit + (s & 1), 1));
+        if (kvdst)  // the incoming ring block joins the KV buffer
+          XCUDA(xdit::launch_kv_place(curK, curV, kvdst, B, Hh, P.S_blk[nsrc], kv_total, segs_of(nsrc), D,
+                                      int64_t(P.S_blk[nsrc]) * row, row, D, eb, st));
       }
+    }
+    if (kvo.buf) {  // every fresh block of the SP group is in the buffer: attend over all of it
+      a.o = dst; a.lse = dst_lse; a.omap = fmap; a.out_f32 = dtype;
+      XRET(buf_attention(a));
+      XRET(mk.rec(pf.t_step[P.r - 1], st));
     }
   }
 
   // ---- a9-a10: reverse all-to-all of O (+ LSE) and unpack into the caller's layout
   if (P.u > 1) {
-    if (peer) {  // the final epilogue already stored chunk p in peer p's receive buffer: flag, wait
-      for (int p = 0; p < P.u; ++p)
-        if (p != P.j) XRET(post_flag(st, static_cast<uint32_t*>(c->peer[i * P.u + p].ptr[kHFlags]) + kFO + P.j, 1));
-      for (int p = 0; p < P.u; ++p)
-        if (p != P.j) {  // peer p sets it again only after my next call's pack (after this reset)
-          XRET(wait_flag(st, c->flags + kFO + p, 1));
-          XRET(post_flag(st, c->flags + kFO + p, 0));
-        }
-    } else {
-      XCUDA(cudaEventRecord(c->ev_o, st));
-      XCUDA(cudaStreamWaitEvent(c->side, c->ev_o, 0));
-      XRET(a2a(c->uly, P.u, c->osend.p, c->orecv.p, need.ochunk, c->side));
-      XCUDA(cudaEventRecord(c->ev_o_a2a, c->side));
-      XCUDA(cudaStreamWaitEvent(st, c->ev_o_a2a, 0));
+    const size_t oc = need.ochunk;
+    XCUDA(cudaMemcpyAsync(static_cast<char*>(c->orecv.p) + P.j * oc, static_cast<const char*>(c->osend.p) + P.j * oc,
+                          oc, cudaMemcpyDeviceToDevice, st));
+    XNCCL(ncclGroupStart());
+    for (int p = 0; p < P.u; ++p) {
+      if (p == P.j) continue;
+      XNCCL(ncclSend(static_cast<const char*>(c->osend.p) + p * oc, oc, ncclUint8, p, c->uly, st));
+      XNCCL(ncclRecv(static_cast<char*>(c->orecv.p) + p * oc, oc, ncclUint8, p, c->uly, st));
     }
+    XNCCL(ncclGroupEnd());
+    pf.ph.a2a_out_bytes = int64_t(P.u - 1) * int64_t(oc);
     XCUDA(xdit::launch_uly_unpack_out(
         c->orecv.p,
         reinterpret_cast<const float*>(static_cast<const char*>(c->orecv.p) + need.ochunk_o),
-        int64_t(need.ochunk), int64_t(need.ochunk), out, lse, B, L, P.Lmax, Hh, D, P.u, eb, st));
+        int64_t(oc), int64_t(oc), out, lse, B, L, P.Lmax, Hh, D, P.u, eb, st));
   }
+  XRET(mk.rec(pf.t_end, st));
   return XDIT_OK;
+}
+
+int prof_make(Prof& p) {
+  if (p.made) return XDIT_OK;
+  cudaEvent_t* evs[3 + 3 * 8];
+  int n = 0;
+  evs[n++] = &p.t0;
+  evs[n++] = &p.t_a2a;
+  evs[n++] = &p.t_end;
+  for (int s = 0; s < 8; ++s) {
+    evs[n++] = &p.t_step[s];
+    evs[n++] = &p.c0[s];
+    evs[n++] = &p.c1[s];
+  }
+  for (int x = 0; x < n; ++x) XCUDA(cudaEventCreate(evs[x]));
+  p.made = true;
+  return XDIT_OK;
+}
+
+void prof_free(Prof& p) {
+  if (!p.made) return;
+  cudaEvent_t evs[] = {p.t0, p.t_a2a, p.t_end};
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  for (int s = 0; s < 8; ++s) {
+    cudaEventDestroy(p.t_step[s]);
+    cudaEventDestroy(p.c0[s]);
+    cudaEventDestroy(p.c1[s]);
+  }
+  p.made = false;
 }
 
 }  // namespace
@@ -666,7 +626,7 @@ extern "C" {
 
 const char* xdit_last_error(void) { return g_err.c_str(); }
 
-int xdit_version(void) { return 20000; }  // 2.0.0: xdit_rowmap gained the segment table (ABI break)
+int xdit_version(void) { return XDIT_ABI_VERSION; }
 
 uint64_t xdit_launch_count(void) { return xdit::g_launches.load(std::memory_order_relaxed); }
 
@@ -780,167 +740,14 @@ int xdit_comm_create(void* nccl_comm, int ulysses, int ring, xdit_comm_t* out) {
   return XDIT_OK;
 }
 
-int xdit_comm_init_peer(int nranks, int rank, int ulysses, int ring, xdit_comm_t* out) {
-  if (!out || nranks < 1 || rank < 0 || rank >= nranks || ulysses < 1 || ring < 1)
-    return fail(XDIT_ERR_INVALID_ARG, "xdit_comm_init_peer: bad arguments");
-  if (ulysses * ring != nranks)
-    return fail(XDIT_ERR_COMM_MISMATCH, "ulysses*ring=%d != nranks=%d", ulysses * ring, nranks);
-  auto* c = new xdit_comm_s();
-  c->nranks = nranks;
-  c->rank = rank;
-  c->u = ulysses;
-  c->r = ring;
-  c->transport = XDIT_TRANSPORT_PEER;
-  int rc = comm_finish_init(c);
-  if (rc != XDIT_OK) {
-    xdit_comm_destroy(c);
-    return rc;
-  }
-  *out = c;
-  return XDIT_OK;
-}
-
-int xdit_comm_transport(xdit_comm_t c) { return c ? c->transport : -1; }
-
-int xdit_comm_peer_export(xdit_comm_t c, void* blob) {
-  if (!c || !blob) return fail(XDIT_ERR_INVALID_ARG, "xdit_comm_peer_export: NULL argument");
-  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
-  PeerBlob b{};
-  b.magic = kBlobMagic;
-  b.rank = c->rank;
-  b.nranks = c->nranks;
-  b.u = c->u;
-  b.r = c->r;
-  b.device = c->device;
-  b.pid = int32_t(getpid());
-  for (int k = 0; k < kNHandles; ++k) {
-    void* p = k == kHFlags ? static_cast<void*>(c->flags) : exported(c, k)->p;
-    if (!p) continue;
-    XCUDA(cudaIpcGetMemHandle(&b.h[k], p));
-    b.bytes[k] = k == kHFlags ? kFlagWords * sizeof(uint32_t) : exported(c, k)->bytes;
-    b.valid |= 1u << k;
-  }
-  std::memset(blob, 0, XDIT_PEER_BLOB_BYTES);
-  std::memcpy(blob, &b, sizeof b);
-  return XDIT_OK;
-}
-
-int xdit_comm_peer_connect(xdit_comm_t c, const void* blobs) {
-  if (!c || !blobs) return fail(XDIT_ERR_INVALID_ARG, "xdit_comm_peer_connect: NULL argument");
-  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
-  std::vector<PeerBlob> bl(c->nranks);
-  for (int q = 0; q < c->nranks; ++q) {
-    std::memcpy(&bl[q], static_cast<const char*>(blobs) + size_t(q) * XDIT_PEER_BLOB_BYTES, sizeof(PeerBlob));
-    const PeerBlob& b = bl[q];
-    if (b.magic != kBlobMagic || b.rank != q || b.nranks != c->nranks || b.u != c->u || b.r != c->r)
-      return fail(XDIT_ERR_COMM_MISMATCH, "peer blob %d is not rank %d of this (%d x %d) mesh", q, q, c->u, c->r);
-    if (q != c->rank && b.pid == int32_t(getpid()))
-      return fail(XDIT_ERR_UNSUPPORTED, "ranks %d and %d live in one process (one process per rank)", q, c->rank);
-  }
-  XCUDA(cudaDeviceSynchronize());
-  close_peers(c);
-  c->peer.assign(c->nranks, PeerMap{});
-  const int i = c->rank / c->u, j = c->rank % c->u;
-  const int nxt = ((i + 1) % c->r) * c->u + j;
-  for (int q = 0; q < c->nranks; ++q) {
-    PeerMap& m = c->peer[q];
-    const bool uly_peer = q / c->u == i && c->u > 1;
-    for (int k = 0; k < kNHandles; ++k) {
-      const bool want = (k == kHFlags || k == kHMbox) ? true  // any rank may message any rank
-                                     : (k < kHKV ? uly_peer : (c->r > 1 && q == nxt));
-      if (!want || !(bl[q].valid & (1u << k))) continue;
-      m.bytes[k] = bl[q].bytes[k];
-      if (q == c->rank) {
-        m.ptr[k] = k == kHFlags ? static_cast<void*>(c->flags) : exported(c, k)->p;
-        continue;
-      }
-      cudaError_t e = cudaIpcOpenMemHandle(&m.ptr[k], bl[q].h[k], cudaIpcMemLazyEnablePeerAccess);
-      if (e != cudaSuccess) {
-        m.ptr[k] = nullptr;
-        close_peers(c);
-        return fail(XDIT_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d, buffer %d): %s", q, k, cudaGetErrorString(e));
-      }
-      m.opened[k] = true;
-    }
-  }
-  c->connected = true;
-  return XDIT_OK;
-}
-
-int xdit_comm_mailbox_reserve(xdit_comm_t c, size_t bytes_per_src) {
-  if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
-  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
-  const size_t region = (bytes_per_src + 255) & ~size_t(255);
-  if (region <= c->mbox_region) return XDIT_OK;
-  XCUDA(cudaDeviceSynchronize());  // peers' writes into the old mailbox drained (caller: after a barrier)
-  XRET(ensure(&c->mbox, region * c->nranks));
-  c->mbox_region = region;
-  c->connected = false;  // peers must map the new mailbox
-  return XDIT_OK;
-}
-
-int xdit_p2p_mailbox(xdit_comm_t c, int src, void** ptr, size_t* bytes) {
-  if (!c || !ptr || src < 0 || src >= c->nranks) return fail(XDIT_ERR_INVALID_ARG, "xdit_p2p_mailbox: bad arguments");
-  if (!c->mbox.p) return fail(XDIT_ERR_WORKSPACE, "no mailbox reserved (xdit_comm_mailbox_reserve)");
-  *ptr = static_cast<char*>(c->mbox.p) + size_t(src) * c->mbox_region;
-  if (bytes) *bytes = c->mbox_region;
-  return XDIT_OK;
-}
-
-namespace {
-int p2p_check(xdit_comm_s* c, int peer_rank) {
-  if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
-  if (c->transport != XDIT_TRANSPORT_PEER) return fail(XDIT_ERR_INVALID_ARG, "handle does not use the peer transport");
-  if (!c->connected) return fail(XDIT_ERR_NOT_CONNECTED, "peer transport: connect after (re)reserving");
-  if (peer_rank < 0 || peer_rank >= c->nranks) return fail(XDIT_ERR_INVALID_ARG, "rank %d out of range", peer_rank);
-  return XDIT_OK;
-}
-}  // namespace
-
-int xdit_p2p_put(xdit_comm_t c, int dst, const void* src, size_t bytes, size_t dst_off, uint32_t tag,
-                 xdit_stream_t stream) {
-  XRET(p2p_check(c, dst));
-  if (!src && bytes) return fail(XDIT_ERR_INVALID_ARG, "xdit_p2p_put: src is NULL");
-  if (dst_off + bytes > c->mbox_region)
-    return fail(XDIT_ERR_WORKSPACE, "xdit_p2p_put: %zu bytes at offset %zu exceed the %zu-byte mailbox region", bytes,
-                dst_off, c->mbox_region);
-  const PeerMap& m = c->peer[dst];
-  if (!m.ptr[kHMbox] || !m.ptr[kHFlags]) return fail(XDIT_ERR_WORKSPACE, "rank %d has no mapped mailbox", dst);
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-  if (bytes)
-    XCUDA(cudaMemcpyAsync(static_cast<char*>(m.ptr[kHMbox]) + size_t(c->rank) * c->mbox_region + dst_off, src, bytes,
-                          cudaMemcpyDefault, st));
-  return post_flag(st, static_cast<uint32_t*>(m.ptr[kHFlags]) + kFP2P + c->rank, tag);
-}
-
-int xdit_p2p_wait(xdit_comm_t c, int src, uint32_t tag, xdit_stream_t stream) {
-  XRET(p2p_check(c, src));
-  return wait_flag(reinterpret_cast<cudaStream_t>(stream), c->flags + kFP2P + src, tag);
-}
-
-int xdit_p2p_ack(xdit_comm_t c, int sender, uint32_t tag, xdit_stream_t stream) {
-  XRET(p2p_check(c, sender));
-  const PeerMap& m = c->peer[sender];
-  if (!m.ptr[kHFlags]) return fail(XDIT_ERR_WORKSPACE, "rank %d's flags are not mapped", sender);
-  return post_flag(reinterpret_cast<cudaStream_t>(stream), static_cast<uint32_t*>(m.ptr[kHFlags]) + kFAck + c->rank,
-                   tag);
-}
-
-int xdit_p2p_wait_ack(xdit_comm_t c, int receiver, uint32_t tag, xdit_stream_t stream) {
-  XRET(p2p_check(c, receiver));
-  return wait_flag(reinterpret_cast<cudaStream_t>(stream), c->flags + kFAck + receiver, tag);
-}
-
 int xdit_comm_reserve(xdit_comm_t c, int B, int H, int S_txt, int S_img, int D, int elem_bytes) {
   if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
   if (elem_bytes != 2 && elem_bytes != 4) return fail(XDIT_ERR_UNSUPPORTED, "elem_bytes must be 2 or 4");
   Plan P;
   XRET(make_plan(B, H, S_txt, S_img, D, c->u, c->r, c->rank, &P));
   const Sizes s = sizes_for(P, B, D, elem_bytes);
-  void* before[kNHandles] = {};
-  for (int k = 0; k < kHFlags; ++k) before[k] = exported(c, k)->p;  // (the mailbox is not reallocated here)
-  if (c->transport == XDIT_TRANSPORT_PEER) XCUDA(cudaDeviceSynchronize());  // peers' writes drained
-  XRET(ensure(&c->uly_send, s.uly3 * (c->transport == XDIT_TRANSPORT_NCCL)));
+  XCUDA(cudaStreamSynchronize(c->side));  // no ring transfer may still use a buffer being replaced
+  XRET(ensure(&c->uly_send, s.uly3));
   XRET(ensure(&c->uly_recv, s.uly3));
   XRET(ensure(&c->qblk, s.qblk));
   for (int a = 0; a < 2; ++a)
@@ -952,8 +759,6 @@ int xdit_comm_reserve(xdit_comm_t c, int B, int H, int S_txt, int S_img, int D, 
   XRET(ensure(&c->osend, s.ochunk * P.u * (P.u > 1)));
   XRET(ensure(&c->orecv, s.ochunk * P.u * (P.u > 1)));
   if (elem_bytes == 2) XRET(ensure(&c->tail, xdit::attn_scratch_floats(D) * sizeof(float)));
-  for (int k = 0; k < kHFlags; ++k)
-    if (exported(c, k)->p != before[k]) c->connected = false;  // peers must map the new buffers
   return XDIT_OK;
 }
 
@@ -969,23 +774,77 @@ int xdit_comm_info(xdit_comm_t c, int* nranks, int* rank, int* ulysses, int* rin
 int xdit_comm_destroy(xdit_comm_t c) {
   if (!c) return XDIT_OK;
   if (c->side) cudaStreamSynchronize(c->side);
-  if (c->transport == XDIT_TRANSPORT_PEER) cudaDeviceSynchronize();
-  close_peers(c);
-  if (c->flags) cudaFree(c->flags);
+  cudaDeviceSynchronize();  // no kernel or NCCL operation of this handle still in flight
   Buf* bufs[] = {&c->uly_send, &c->uly_recv, &c->qblk, &c->kv[0][0], &c->kv[0][1], &c->kv[1][0],
-                 &c->kv[1][1], &c->oacc, &c->lacc, &c->otmp, &c->ltmp, &c->osend, &c->orecv, &c->tail,
-                 &c->mbox};
+                 &c->kv[1][1], &c->oacc, &c->lacc, &c->otmp, &c->ltmp, &c->osend, &c->orecv, &c->tail};
   for (Buf* b : bufs)
     if (b->p) cudaFree(b->p);
   if (c->uly) ncclCommDestroy(c->uly);
   if (c->ring) ncclCommDestroy(c->ring);
+  if (c->all && c->all != c->sp) ncclCommDestroy(c->all);
   if (c->sp && c->own_sp) ncclCommDestroy(c->sp);
-  cudaEvent_t evs[] = {c->ev_start, c->ev_a2a, c->ev_o, c->ev_o_a2a,
-                       c->ev_kdone[0], c->ev_kdone[1], c->ev_recv[0], c->ev_recv[1]};
+  cudaEvent_t evs[] = {c->ev_fork, c->ev_recv[0], c->ev_recv[1]};
   for (cudaEvent_t e : evs)
     if (e) cudaEventDestroy(e);
+  prof_free(c->prof);
   if (c->side) cudaStreamDestroy(c->side);
   delete c;
+  return XDIT_OK;
+}
+
+int xdit_p2p(xdit_comm_t c, const xdit_p2p_op* ops, int n, xdit_stream_t stream) {
+  if (!c || n < 0 || (n > 0 && !ops)) return fail(XDIT_ERR_INVALID_ARG, "xdit_p2p: bad arguments");
+  for (int x = 0; x < n; ++x) {
+    if (ops[x].peer < 0 || ops[x].peer >= c->nranks || (ops[x].bytes && !ops[x].buf))
+      return fail(XDIT_ERR_INVALID_ARG, "xdit_p2p: op %d (peer %d, %zu bytes) invalid for %d ranks", x, ops[x].peer,
+                  ops[x].bytes, c->nranks);
+    if (ops[x].peer == c->rank && ops[x].bytes)
+      return fail(XDIT_ERR_INVALID_ARG, "xdit_p2p: op %d addresses this rank itself", x);
+  }
+  if (n == 0 || c->nranks == 1) return XDIT_OK;
+  XRET(check_async(c));
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  XNCCL(ncclGroupStart());
+  for (int x = 0; x < n; ++x) {
+    if (!ops[x].bytes) continue;
+    if (ops[x].is_send)
+      XNCCL(ncclSend(ops[x].buf, ops[x].bytes, ncclUint8, ops[x].peer, c->all, st));
+    else
+      XNCCL(ncclRecv(ops[x].buf, ops[x].bytes, ncclUint8, ops[x].peer, c->all, st));
+  }
+  XNCCL(ncclGroupEnd());
+  return XDIT_OK;
+}
+
+int xdit_comm_profile(xdit_comm_t c, int enable) {
+  if (!c) return fail(XDIT_ERR_INVALID_ARG, "comm handle is NULL");
+  if (enable) XRET(prof_make(c->prof));
+  c->prof.on = enable != 0;
+  c->prof.recorded = false;
+  return XDIT_OK;
+}
+
+int xdit_comm_phases(xdit_comm_t c, xdit_phases* out) {
+  if (!c || !out) return fail(XDIT_ERR_INVALID_ARG, "xdit_comm_phases: NULL argument");
+  Prof& p = c->prof;
+  *out = p.ph;
+  out->valid = 0;
+  if (!p.recorded) return XDIT_OK;
+  XCUDA(cudaEventSynchronize(p.t_end));
+  const int rs = c->r;
+  for (int s = 0; s < rs - 1 && s < 8; ++s) XCUDA(cudaEventSynchronize(p.c1[s]));
+  auto el = [](cudaEvent_t a, cudaEvent_t b, float* ms) -> int {
+    XCUDA(cudaEventElapsedTime(ms, a, b));
+    return XDIT_OK;
+  };
+  XRET(el(p.t0, p.t_end, &out->total_ms));
+  XRET(el(p.t0, p.t_a2a, &out->a2a_in_ms));
+  XRET(el(p.t_step[rs - 1], p.t_end, &out->a2a_out_ms));
+  for (int s = 0; s < rs && s < 8; ++s) {
+    XRET(el(s == 0 ? p.t_a2a : p.t_step[s - 1], p.t_step[s], &out->attn_ms[s]));
+    if (s < rs - 1) XRET(el(p.c0[s], p.c1[s], &out->ring_comm_ms[s]));
+  }
+  out->valid = 1;
   return XDIT_OK;
 }
 
@@ -1007,8 +866,24 @@ int xdit_usp_attention_kv(const void* q, const void* k, const void* v, void* out
                           int B, int H, int S_txt, int S_img, int D, int ulysses, int ring,
                           xdit_stream_t stream, xdit_comm_t comm) {
   if (!kv_keep) return fail(XDIT_ERR_INVALID_ARG, "kv_keep must not be NULL (use xdit_usp_attention)");
+  KvOpts o;
+  o.keep = kv_keep;
   return usp_call(q, k, v, out, lse, B, H, S_txt, S_img, D, ulysses, ring,
-                  reinterpret_cast<cudaStream_t>(stream), comm, 2, kv_keep);
+                  reinterpret_cast<cudaStream_t>(stream), comm, 2, o);
+}
+
+int xdit_usp_attention_buf(const void* q, const void* k, const void* v, void* out, float* lse, void* kv_buf, int B,
+                           int H, int S_txt, int S_img, int D, int ulysses, int ring, int S_buf, int txt_row,
+                           int img_row, int dtype, xdit_stream_t stream, xdit_comm_t comm) {
+  if (!kv_buf) return fail(XDIT_ERR_INVALID_ARG, "kv_buf must not be NULL");
+  if (dtype != 0 && dtype != 1) return fail(XDIT_ERR_UNSUPPORTED, "dtype must be 0 (bf16) or 1 (fp32)");
+  KvOpts o;
+  o.buf = kv_buf;
+  o.S_buf = S_buf;
+  o.txt_row = txt_row;
+  o.img_row = img_row;
+  return usp_call(q, k, v, out, lse, B, H, S_txt, S_img, D, ulysses, ring,
+                  reinterpret_cast<cudaStream_t>(stream), comm, dtype == 0 ? 2 : 4, o);
 }
 
 int xdit_kv_retain(const void* k_blk, const void* v_blk, void* kv_keep, int B, int Hh, int S_blk, int S_total,
@@ -1056,37 +931,8 @@ int xdit_cfg_tail(const void* eps_local, void* eps_gather, void* eps_out, int64_
   XRET(check_async(comm));
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   // All-gather of the two branches' predictions over the cfg pair (rank 0 = conditional, rank 1 =
-  // unconditional: reading R3), then the combine on every rank.
-  const size_t bytes = size_t(n) * eb;
-  if (comm->transport == XDIT_TRANSPORT_PEER) {
-    // peer transport: eps_local -> the peer's mailbox (after the peer acknowledged the previous
-    // call's), flag; own copy into eps_gather[rank]; wait for the peer's flag, copy its prediction out
-    // of the mailbox into eps_gather[1 - rank], acknowledge.
-    if (!comm->connected) return fail(XDIT_ERR_NOT_CONNECTED, "peer transport: connect after (re)reserving");
-    if (bytes > comm->mbox_region)
-      return fail(XDIT_ERR_WORKSPACE, "cfg_tail: %zu bytes exceed the %zu-byte mailbox region "
-                  "(xdit_comm_mailbox_reserve)", bytes, comm->mbox_region);
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    XCUDA(cudaStreamIsCapturing(st, &cs));
-    if (cs != cudaStreamCaptureStatusNone)  // its flags carry per-call epochs (immediates)
-      return fail(XDIT_ERR_UNSUPPORTED, "cfg_tail over the peer transport cannot be captured in a CUDA graph");
-    const int me = comm->rank, other = 1 - me;
-    const uint32_t e = ++comm->cfg_epoch;
-    const PeerMap& m = comm->peer[other];
-    char* gb = static_cast<char*>(eps_gather);
-    XRET(wait_flag(st, comm->flags + kFCfgAck + other, e - 1));
-    XCUDA(cudaMemcpyAsync(static_cast<char*>(m.ptr[kHMbox]) + size_t(me) * comm->mbox_region, eps_local, bytes,
-                          cudaMemcpyDefault, st));
-    XRET(post_flag(st, static_cast<uint32_t*>(m.ptr[kHFlags]) + kFCfg + me, e));
-    XCUDA(cudaMemcpyAsync(gb + size_t(me) * bytes, eps_local, bytes, cudaMemcpyDeviceToDevice, st));
-    XRET(wait_flag(st, comm->flags + kFCfg + other, e));
-    XCUDA(cudaMemcpyAsync(gb + size_t(other) * bytes, static_cast<char*>(comm->mbox.p) + size_t(other) * comm->mbox_region,
-                          bytes, cudaMemcpyDeviceToDevice, st));
-    XRET(post_flag(st, static_cast<uint32_t*>(m.ptr[kHFlags]) + kFCfgAck + me, e));
-    XCUDA(xdit::launch_cfg_combine(gb, gb + bytes, eps_out, n, g, dtype, st));
-    return XDIT_OK;
-  }
-  XNCCL(ncclAllGather(eps_local, eps_gather, size_t(n) * eb, ncclUint8, comm->sp, st));
+  // unconditional: reading R3) on the handle's private communicator, then the combine on every rank.
+  XNCCL(ncclAllGather(eps_local, eps_gather, size_t(n) * eb, ncclUint8, comm->all, st));
   const char* gb = static_cast<const char*>(eps_gather);
   XCUDA(xdit::launch_cfg_combine(gb, gb + size_t(n) * eb, eps_out, n, g, dtype, st));
   return XDIT_OK;
@@ -1120,6 +966,26 @@ int xdit_pf_sampler(void* x, const void* eps, int64_t n, float sigma, int dtype,
   if (!x || !eps || n < 0 || (dtype != 0 && dtype != 1)) return fail(XDIT_ERR_INVALID_ARG, "xdit_pf_sampler: bad arguments");
   if (!aligned16(x) || !aligned16(eps) || n % 8) return fail(XDIT_ERR_ALIGNMENT, "xdit_pf_sampler: 16-byte alignment, n %% 8 == 0");
   XCUDA(xdit::launch_pf_sampler(x, eps, n, sigma, dtype, reinterpret_cast<cudaStream_t>(stream)));
+  return XDIT_OK;
+}
+
+int xdit_pf_qkv(const void* h, const float* w, void* q, void* k, void* v, int B, int n, int H, int D, int dtype,
+                xdit_stream_t stream) {
+  if (!h || !w || !q || !k || !v || B < 0 || n < 0 || H < 1 || D < 1 || (dtype != 0 && dtype != 1))
+    return fail(XDIT_ERR_INVALID_ARG, "xdit_pf_qkv: bad arguments");
+  if (D % 8 || !aligned16(h) || !aligned16(w) || !aligned16(q) || !aligned16(k) || !aligned16(v))
+    return fail(XDIT_ERR_ALIGNMENT, "xdit_pf_qkv: D %% 8 == 0 and 16-byte aligned pointers required");
+  XCUDA(xdit::launch_pf_qkv(h, w, q, k, v, B, n, H, D, dtype, reinterpret_cast<cudaStream_t>(stream)));
+  return XDIT_OK;
+}
+
+int xdit_pf_residual(void* h, const void* o, const float* w, int B, int n, int H, int D, int dtype,
+                     xdit_stream_t stream) {
+  if (!h || !o || !w || B < 0 || n < 0 || H < 1 || D < 1 || (dtype != 0 && dtype != 1))
+    return fail(XDIT_ERR_INVALID_ARG, "xdit_pf_residual: bad arguments");
+  if (D % 8 || !aligned16(h) || !aligned16(o) || !aligned16(w))
+    return fail(XDIT_ERR_ALIGNMENT, "xdit_pf_residual: D %% 8 == 0 and 16-byte aligned pointers required");
+  XCUDA(xdit::launch_pf_residual(h, o, w, B, n, H, D, dtype, reinterpret_cast<cudaStream_t>(stream)));
   return XDIT_OK;
 }
 
@@ -1204,7 +1070,7 @@ int xdit_lse_merge(float* o_acc, float* lse_acc, const float* o_s, const float* 
 
 int xdit_uly_pack(const void* x, void* send, int B, int L, int Lmax, int H, int D, int u, int slot,
                   int nslots, int elem_bytes, xdit_stream_t stream) {
-  if (!x || !send || B < 0 || L < 0 || Lmax < L || H <= 0 || D <= 0 || u < 1 || H % u != 0 ||
+  if (!x || !send || B < 0 || L < 0 || Lmax < L || H <= 0 || D <= 0 || u < 1 || u > 8 || H % u != 0 ||
       slot < 0 || slot >= nslots || (elem_bytes != 2 && elem_bytes != 4))
     return fail(XDIT_ERR_INVALID_ARG, "xdit_uly_pack: bad arguments");
   XCUDA(xdit::launch_uly_pack(x, send, B, L, Lmax, H, D, u, slot, nslots, elem_bytes,

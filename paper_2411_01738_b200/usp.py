@@ -3,6 +3,8 @@
 Argument marshalling only: torch tensors -> device pointers, the current CUDA stream -> handle,
 status codes -> exceptions.  Every step of the hot path runs in the library's CUDA kernels and
 NCCL; there is no Python or CPU fallback -- if the extension is missing this module raises.
+The binding refuses a library whose xdit_version() differs from ABI_VERSION (the struct layouts
+below are those of include/xdit_usp.h at that version).
 """
 from __future__ import annotations
 
@@ -13,11 +15,10 @@ from typing import Optional, Sequence, Tuple
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("XDIT_LIB") or os.path.join(HERE, "libxdit_usp.so")  # XDIT_LIB: A/B builds
 
+ABI_VERSION = 30000  # XDIT_ABI_VERSION of include/xdit_usp.h
 XDIT_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "DIVISIBILITY", 4: "COMM_MISMATCH",
-               5: "EMPTY_SHARD", 6: "ALIGNMENT", 7: "CUDA", 8: "NCCL", 9: "WORKSPACE", 10: "NOT_CONNECTED"}
+               5: "EMPTY_SHARD", 6: "ALIGNMENT", 7: "CUDA", 8: "NCCL", 9: "WORKSPACE"}
 NCCL_UNIQUE_ID_BYTES = 128
-PEER_BLOB_BYTES = 1024  # XDIT_PEER_BLOB_BYTES
-TRANSPORTS = {"nccl": 0, "peer": 1}  # XDIT_TRANSPORT_NCCL / XDIT_TRANSPORT_PEER
 
 
 class XditError(RuntimeError):
@@ -32,8 +33,7 @@ class RowMap(ctypes.Structure):
     _fields_ = [("nseg", ctypes.c_int32), ("seg_off", ctypes.c_int32 * 9),
                 ("o_seg", ctypes.c_int64), ("o_b", ctypes.c_int64), ("o_s", ctypes.c_int64),
                 ("o_h", ctypes.c_int64), ("l_seg", ctypes.c_int64), ("l_b", ctypes.c_int64),
-                ("l_h", ctypes.c_int64), ("o_seg_off", ctypes.c_int64 * 8), ("l_seg_off", ctypes.c_int64 * 8),
-                ("seg_table", ctypes.c_int32)]
+                ("l_h", ctypes.c_int64)]
 
     @classmethod
     def plain(cls, B: int, S: int, H: int, D: int) -> "RowMap":
@@ -57,6 +57,28 @@ class Plan(ctypes.Structure):
                 ("a2a_bytes_per_peer", ctypes.c_int64), ("ring_bytes", ctypes.c_int64 * 8)]
 
 
+class P2POp(ctypes.Structure):
+    """xdit_p2p_op: one send or receive of an xdit_p2p group."""
+    _fields_ = [("peer", ctypes.c_int32), ("is_send", ctypes.c_int32), ("buf", ctypes.c_void_p),
+                ("bytes", ctypes.c_size_t)]
+
+
+class Phases(ctypes.Structure):
+    """xdit_phases: per-phase timing of the last profiled xdit_usp_attention call."""
+    _fields_ = [("valid", ctypes.c_int32), ("ulysses", ctypes.c_int32), ("ring", ctypes.c_int32),
+                ("pad_", ctypes.c_int32), ("total_ms", ctypes.c_float), ("a2a_in_ms", ctypes.c_float),
+                ("a2a_out_ms", ctypes.c_float), ("pad2_", ctypes.c_float), ("attn_ms", ctypes.c_float * 8),
+                ("ring_comm_ms", ctypes.c_float * 8), ("a2a_in_bytes", ctypes.c_int64),
+                ("a2a_out_bytes", ctypes.c_int64), ("ring_bytes", ctypes.c_int64 * 8)]
+
+    def as_dict(self):
+        r = self.ring
+        return {"total_ms": self.total_ms, "a2a_in_ms": self.a2a_in_ms, "a2a_out_ms": self.a2a_out_ms,
+                "attn_ms": list(self.attn_ms[:r]), "ring_comm_ms": list(self.ring_comm_ms[:max(0, r - 1)]),
+                "a2a_in_bytes": int(self.a2a_in_bytes), "a2a_out_bytes": int(self.a2a_out_bytes),
+                "ring_bytes": [int(x) for x in self.ring_bytes[:max(0, r - 1)]]}
+
+
 _lib = None
 _vp, _i, _i64, _fp = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p
 
@@ -69,22 +91,16 @@ _SIGS = {
     "xdit_nccl_unique_id": ([_vp], _i),
     "xdit_comm_init": ([_vp, _i, _i, _i, _i, ctypes.POINTER(_vp)], _i),
     "xdit_comm_create": ([_vp, _i, _i, ctypes.POINTER(_vp)], _i),
-    "xdit_comm_init_peer": ([_i, _i, _i, _i, ctypes.POINTER(_vp)], _i),
-    "xdit_comm_peer_export": ([_vp, _vp], _i),
-    "xdit_comm_peer_connect": ([_vp, _vp], _i),
-    "xdit_comm_transport": ([_vp], _i),
-    "xdit_comm_mailbox_reserve": ([_vp, ctypes.c_size_t], _i),
-    "xdit_p2p_mailbox": ([_vp, _i, ctypes.POINTER(_vp), ctypes.POINTER(ctypes.c_size_t)], _i),
-    "xdit_p2p_put": ([_vp, _i, _vp, ctypes.c_size_t, ctypes.c_size_t, ctypes.c_uint32, _vp], _i),
-    "xdit_p2p_wait": ([_vp, _i, ctypes.c_uint32, _vp], _i),
-    "xdit_p2p_ack": ([_vp, _i, ctypes.c_uint32, _vp], _i),
-    "xdit_p2p_wait_ack": ([_vp, _i, ctypes.c_uint32, _vp], _i),
+    "xdit_p2p": ([_vp, ctypes.POINTER(P2POp), _i, _vp], _i),
+    "xdit_comm_profile": ([_vp, _i], _i),
+    "xdit_comm_phases": ([_vp, ctypes.POINTER(Phases)], _i),
     "xdit_comm_reserve": ([_vp, _i, _i, _i, _i, _i, _i], _i),
     "xdit_comm_info": ([_vp] + [ctypes.POINTER(_i)] * 4, _i),
     "xdit_comm_destroy": ([_vp], _i),
     "xdit_usp_attention": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
     "xdit_usp_attention_f32": ([_vp] * 5 + [_i] * 7 + [_vp, _vp], _i),
     "xdit_usp_attention_kv": ([_vp] * 6 + [_i] * 7 + [_vp, _vp], _i),
+    "xdit_usp_attention_buf": ([_vp] * 6 + [_i] * 11 + [_vp, _vp], _i),
     "xdit_cfg_combine": ([_vp, _vp, _vp, _i64, ctypes.c_float, _i, _vp], _i),
     "xdit_cfg_tail": ([_vp, _vp, _vp, _i64, ctypes.c_float, _i, _vp, _vp], _i),
     "xdit_kv_retain": ([_vp, _vp, _vp] + [_i] * 6 + [_i64] * 3 + [_i, _vp], _i),
@@ -98,6 +114,8 @@ _SIGS = {
     "xdit_pf_block_workspace_bytes": ([_i] * 5, ctypes.c_size_t),
     "xdit_pf_block": ([_vp] * 4 + [ctypes.c_size_t] + [_i] * 7 + [_vp], _i),
     "xdit_pf_sampler": ([_vp, _vp, _i64, ctypes.c_float, _i, _vp], _i),
+    "xdit_pf_qkv": ([_vp] * 5 + [_i] * 5 + [_vp], _i),
+    "xdit_pf_residual": ([_vp] * 3 + [_i] * 5 + [_vp], _i),
     "xdit_vae_conv3x3": ([_vp, _i, _i, _i, _vp, _vp, _vp, _i, _i, _vp], _i),
     "xdit_vae_conv3x3_bf16": ([_vp, _i, _i, _i, _vp, _vp, _vp, _i, _i, _vp], _i),
 }
@@ -115,6 +133,8 @@ def lib():
             fn = getattr(L, name)
             fn.argtypes = args
             fn.restype = res
+        if L.xdit_version() != ABI_VERSION:
+            raise ImportError(f"{LIB_PATH} has ABI {L.xdit_version()}, this binding needs {ABI_VERSION}: rebuild it")
         _lib = L
     return _lib
 
@@ -169,24 +189,38 @@ def _stream(stream=None) -> int:
     return s.cuda_stream
 
 
+def _torch_nccl_comm(group):
+    """The ncclComm_t of a torch ProcessGroupNCCL (its `_comm_ptr()`), or None for another backend.
+    torch creates a group's communicator lazily; a 1-element all_reduce forces it into existence."""
+    import torch
+    import torch.distributed as dist
+    pg = group if group is not None else dist.distributed_c10d._get_default_group()
+    if dist.get_backend(pg) != "nccl":
+        return None
+    be = pg._get_backend(torch.device("cuda", torch.cuda.current_device()))
+    ptr = be._comm_ptr() if hasattr(be, "_comm_ptr") else 0
+    if not ptr:
+        t = torch.zeros(1, device="cuda")
+        dist.all_reduce(t, group=pg)
+        torch.cuda.synchronize()
+        ptr = be._comm_ptr()
+    return int(ptr) or None
+
+
 class Comm:
-    """One SP group (= one CFG group): ulysses x ring mesh, transport, workspace.
+    """One SP group (= one CFG group): ulysses x ring mesh, NCCL communicators, workspace.
 
-    transport="peer" (default): the library's peer-memory transport -- ranks map each other's
-    receive buffers (CUDA IPC over NVLink/NVSwitch) and order their streams with device flags;
-    torch.distributed (`group`, any backend) only carries the one-time handle exchange.
-    transport="nccl": rank 0 of `group` creates an NCCL unique id, broadcast with torch.distributed,
-    and every rank calls xdit_comm_init (the library's own NCCL communicators).
-    With ulysses*ring == 1 neither is needed and no communication object is made.
-    """
+    Every byte between ranks moves over NCCL.  If `group` (torch.distributed, default: the world) is
+    an NCCL process group, the handle splits that group's own communicator (`pg._comm_ptr()` ->
+    xdit_comm_create); otherwise (e.g. a gloo group carrying only host plumbing) rank
+    0 creates an NCCL unique id, torch.distributed broadcasts it and every rank calls
+    xdit_comm_init.  With ulysses*ring == 1 no communicator is made."""
 
-    def __init__(self, ulysses: int = 1, ring: int = 1, group=None, transport: str = "peer"):
-        if transport not in TRANSPORTS:
-            raise XditError(1, "Comm", f"transport must be one of {sorted(TRANSPORTS)}, got {transport!r}")
+    def __init__(self, ulysses: int = 1, ring: int = 1, group=None):
         self.ulysses, self.ring, self.group = ulysses, ring, group
         n = ulysses * ring
         h = _vp()
-        self.transport = transport if n > 1 else "nccl"
+        self.source = None
         if n == 1:
             _check(lib().xdit_comm_init(None, 1, 0, 1, 1, ctypes.byref(h)), "xdit_comm_init")
             self.rank = 0
@@ -195,8 +229,10 @@ class Comm:
             rank = dist.get_rank(group)
             if dist.get_world_size(group) != n:
                 raise XditError(4, "Comm", f"group size {dist.get_world_size(group)} != ulysses*ring={n}")
-            if transport == "peer":
-                _check(lib().xdit_comm_init_peer(n, rank, ulysses, ring, ctypes.byref(h)), "xdit_comm_init_peer")
+            ptr = _torch_nccl_comm(group)
+            if ptr is not None:
+                _check(lib().xdit_comm_create(ptr, ulysses, ring, ctypes.byref(h)), "xdit_comm_create")
+                self.source = "torch ProcessGroupNCCL._comm_ptr()"
             else:
                 buf = (ctypes.c_uint8 * NCCL_UNIQUE_ID_BYTES)()
                 if rank == 0:
@@ -207,88 +243,48 @@ class Comm:
                 ctypes.memmove(buf, obj[0], NCCL_UNIQUE_ID_BYTES)
                 _check(lib().xdit_comm_init(ctypes.cast(buf, _vp), n, rank, ulysses, ring, ctypes.byref(h)),
                        "xdit_comm_init")
+                self.source = "own NCCL communicator (unique id over torch.distributed)"
             self.rank = rank
         self.handle = h
         self._reserved = None
-        # per-channel message counters of mailbox users (PipeFusion stages, VAE bands): the device
-        # flags keep their values across calls, so the tags must continue where the last call ended
-        self.p2p_tags = {}
+
+    @property
+    def size(self) -> int:
+        return self.ulysses * self.ring
 
     def reserve(self, B: int, H: int, S_txt: int, S_img: int, D: int, elem_bytes: int = 2):
-        """Collective when the shape changes (every rank, same scalars): reserve the workspace and,
-        for the peer transport, exchange and map the peers' buffers."""
+        """Workspace for a shape (every rank, same scalars; a no-op when it already fits)."""
         key = (B, H, S_txt, S_img, D, elem_bytes)
         if self._reserved != key:
-            peer = self.transport == "peer"
-            if peer:  # nobody may still be writing into a buffer the reserve could reallocate
-                import torch
-                import torch.distributed as dist
-                torch.cuda.synchronize()
-                dist.barrier(group=self.group)
             _check(lib().xdit_comm_reserve(self.handle, *key), "xdit_comm_reserve")
-            if peer:
-                self.connect()
             self._reserved = key
         return self
 
-    def connect(self):
-        """Peer transport: export this rank's buffer descriptor, all-gather them, map the peers'."""
-        import torch.distributed as dist
-        blob = (ctypes.c_uint8 * PEER_BLOB_BYTES)()
-        _check(lib().xdit_comm_peer_export(self.handle, ctypes.cast(blob, _vp)), "xdit_comm_peer_export")
-        n = self.ulysses * self.ring
-        blobs = [None] * n
-        dist.all_gather_object(blobs, bytes(blob), group=self.group)
-        allb = (ctypes.c_uint8 * (PEER_BLOB_BYTES * n)).from_buffer_copy(b"".join(blobs))
-        _check(lib().xdit_comm_peer_connect(self.handle, ctypes.cast(allb, _vp)), "xdit_comm_peer_connect")
+    def p2p(self, ops, stream=None):
+        """One NCCL group of sends / receives: ops = [(peer, "send" | "recv", tensor), ...]
+        (xdit_p2p; contiguous CUDA tensors, the receiving side's tensor has the same byte size)."""
+        arr = (P2POp * max(1, len(ops)))()
+        for x, (peer, kind, t) in enumerate(ops):
+            if kind not in ("send", "recv"):
+                raise XditError(1, "Comm.p2p", f"op kind must be 'send' or 'recv', got {kind!r}")
+            if not t.is_contiguous():
+                raise XditError(1, "Comm.p2p", "tensors must be contiguous")
+            arr[x] = P2POp(int(peer), 1 if kind == "send" else 0, _ptr(t), t.numel() * t.element_size())
+        _check(lib().xdit_p2p(self.handle, arr, len(ops), _stream(stream)), "xdit_p2p")
 
-    # ---- peer-transport mailbox (point-to-point messages; see include/xdit_usp.h)
-    def mailbox(self, bytes_per_src: int):
-        """Collective: reserve >= bytes_per_src bytes of mailbox per source rank (re-connects)."""
-        import torch
-        import torch.distributed as dist
-        if self.transport != "peer":
-            raise XditError(1, "Comm.mailbox", "the mailbox needs the peer transport")
-        torch.cuda.synchronize()
-        dist.barrier(group=self.group)
-        _check(lib().xdit_comm_mailbox_reserve(self.handle, int(bytes_per_src)), "xdit_comm_mailbox_reserve")
-        self.connect()
-        return self
+    def profile(self, enable: bool = True):
+        """Record per-phase timing events in the following calls (xdit_comm_profile)."""
+        _check(lib().xdit_comm_profile(self.handle, 1 if enable else 0), "xdit_comm_profile")
 
-    def mailbox_view(self, src: int, shape, dtype, offset: int = 0):
-        """Torch view of this rank's mailbox region from rank `src` (no copy)."""
-        import math
-        import torch
-        p, n = _vp(), ctypes.c_size_t()
-        _check(lib().xdit_p2p_mailbox(self.handle, src, ctypes.byref(p), ctypes.byref(n)), "xdit_p2p_mailbox")
-        esz = torch.empty((), dtype=dtype).element_size()
-        if offset + math.prod(shape) * esz > n.value:
-            raise XditError(9, "mailbox_view", "view exceeds the mailbox region")
-        typestr = {torch.bfloat16: "<i2", torch.float32: "<f4", torch.float16: "<f2", torch.uint8: "|u1"}[dtype]
-
-        class _Cai:
-            __cuda_array_interface__ = {"shape": tuple(shape), "typestr": typestr, "data": (p.value + offset, False),
-                                        "version": 3, "strides": None}
-        t = torch.as_tensor(_Cai(), device=torch.device("cuda", torch.cuda.current_device()))
-        return t.view(dtype) if dtype == torch.bfloat16 else t
-
-    def put(self, dst: int, src, tag: int, offset: int = 0, stream=None):
-        n = src.numel() * src.element_size()
-        _check(lib().xdit_p2p_put(self.handle, dst, _ptr(src), n, offset, tag & 0xFFFFFFFF, _stream(stream)),
-               "xdit_p2p_put")
-
-    def wait(self, src: int, tag: int, stream=None):
-        _check(lib().xdit_p2p_wait(self.handle, src, tag & 0xFFFFFFFF, _stream(stream)), "xdit_p2p_wait")
-
-    def ack(self, sender: int, tag: int, stream=None):
-        _check(lib().xdit_p2p_ack(self.handle, sender, tag & 0xFFFFFFFF, _stream(stream)), "xdit_p2p_ack")
-
-    def wait_ack(self, receiver: int, tag: int, stream=None):
-        _check(lib().xdit_p2p_wait_ack(self.handle, receiver, tag & 0xFFFFFFFF, _stream(stream)), "xdit_p2p_wait_ack")
+    def phases(self) -> Optional[dict]:
+        """Per-phase times and bytes of the last profiled call (host-synchronising), or None."""
+        ph = Phases()
+        _check(lib().xdit_comm_phases(self.handle, ctypes.byref(ph)), "xdit_comm_phases")
+        return ph.as_dict() if ph.valid else None
 
     def destroy(self):
-        """Frees the handle.  Peer transport: every rank must have drained its streams first (the
-        peers may still be writing into this rank's buffers) -- call collectively, after a barrier."""
+        """Frees the handle (device-synchronising; collective only in that peers must have finished
+        the calls they share with this rank)."""
         if self.handle:
             lib().xdit_comm_destroy(self.handle)
             self.handle = None
@@ -334,6 +330,29 @@ def attention(q, k, v, *, S_txt: int, S_img: int, comm: Comm, ulysses: int = 1, 
     rc = fn(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), B, H, S_txt, S_img, D, ulysses, ring,
             _stream(stream), comm.handle)
     _check(rc, "xdit_usp_attention_f32" if f32 else "xdit_usp_attention")
+    return out, lse
+
+
+def attention_buf(q, k, v, kv_buf, *, S_txt: int, S_img: int, txt_row: int, img_row: int, comm: Comm,
+                  ulysses: int = 1, ring: int = 1, out=None, lse=None, stream=None):
+    """USP attention of one PipeFusion patch over the persistent KV buffer (xdit_usp_attention_buf,
+    hybrid PipeFusion x SP, NEXT 3): q, k, v this rank's rows of the patch [B, S_loc, H, D] (the
+    patch = S_txt text + S_img image tokens); kv_buf [2, B, H/ulysses, S_buf, D] of the same dtype,
+    the patch's text token t at row txt_row + t, image token t at img_row + t.  Returns (out, lse)."""
+    import torch
+    B, L, H, D = q.shape
+    for t in (q, k, v, kv_buf):
+        if not t.is_cuda or not t.is_contiguous():
+            raise XditError(1, "attention_buf", "q, k, v, kv_buf must be contiguous CUDA tensors")
+    if out is None:
+        out = torch.empty_like(q)
+    f32 = q.dtype == torch.float32
+    comm.reserve(B, H, S_txt, S_img, D, 4 if f32 else 2)
+    S_buf = kv_buf.shape[3]
+    rc = lib().xdit_usp_attention_buf(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(lse), _ptr(kv_buf), B, H, S_txt,
+                                      S_img, D, ulysses, ring, S_buf, txt_row, img_row, 1 if f32 else 0,
+                                      _stream(stream), comm.handle)
+    _check(rc, "xdit_usp_attention_buf")
     return out, lse
 
 

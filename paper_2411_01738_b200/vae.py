@@ -3,7 +3,7 @@
 Host orchestration only: every conv runs in the library -- `xdit_vae_conv3x3` (SIMT fp32,
 activations [H][C][W]) or, with tc=True, `xdit_vae_conv3x3_bf16` (tcgen05 implicit GEMM, bf16
 activations [H][W][C], channels padded to a multiple of 8) -- with the stage's SiLU and x2 upsample
-fused into the store; halo rows move between devices through the peer-transport mailbox.  In both
+fused into the store; halo rows move between devices with xdit_p2p (NCCL).  In both
 layouts a row of the feature map is contiguous.  The decoder: per stage a 3x3 conv + SiLU + nearest
 x2 upsample, then a final 3x3 conv to 3 channels.
 """
@@ -97,41 +97,25 @@ def decode(latent, dec: Decoder):
 
 def decode_band(band, dec: Decoder, comm):
     """Patch-parallel decode, one process per band: this rank (= comm.rank of N) holds latent rows
-    `band` ([h_g][c][w] fp32, or [h_g][w][c'] bf16 for a tc decoder); two mailbox spaces (layer
-    parity) per source hold the halo rows; before every conv it sends its first row to rank g-1 and its last row to rank
-    g+1 (their bottom / top halos) through the mailbox and receives theirs.  Collective.  Returns
-    this rank's band of the decoded image."""
+    `band` ([h_g][c][w] fp32, or [h_g][w][c'] bf16 for a tc decoder).  Before every conv it sends
+    its first row to rank g-1 and its last row to rank g+1 (their bottom / top halos) and receives
+    theirs into its own halo rows -- one xdit_p2p group (NCCL) per conv, "the exchange of the
+    boundary data for convolutional operators"; the image edges keep zero halos (= the
+    serial zero padding).  Collective over the comm's ranks.  Returns this rank's decoded band."""
     import torch
-    N, g = comm.ulysses * comm.ring, comm.rank
+    N, g = comm.size, comm.rank
     st = torch.cuda.current_stream()
-    # a row of the widest layer input ([C][W] fp32 or [W][C'] bf16; the upsampling doubles W)
-    C, W = (band.shape[2], band.shape[1]) if dec.tc else (band.shape[1], band.shape[2])
-    rows = []
-    for i, (w, _) in enumerate(dec.layers):
-        rows.append(C * W * band.element_size())
-        C = _pad8(w.shape[1]) if dec.tc else w.shape[0]
-        W = 2 * W if i < len(dec.layers) - 1 else W
-    rb = (max(rows) + 255) // 256 * 256
-    comm.mailbox(2 * rb)
-    tags = comm.p2p_tags.setdefault("vae", {})
     x = band
     for i, (w, b) in enumerate(dec.layers):
         h = x.shape[0]
-        ext = torch.empty((h + 2,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        ext = torch.zeros((h + 2,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
         ext[1:-1].copy_(x)
-        for nb, row in ((g - 1, x[0]), (g + 1, x[h - 1])):  # my boundary rows -> the neighbours
-            if 0 <= nb < N:
-                t = tags[("out", nb)] = tags.get(("out", nb), 0) + 1
-                if t > 2:
-                    comm.wait_ack(nb, t - 2, stream=st)
-                comm.put(nb, row, t, offset=(t % 2) * rb, stream=st)
-        for nb, dst in ((g - 1, ext[0]), (g + 1, ext[h + 1])):  # the neighbours' rows -> my halos
-            if 0 <= nb < N:
-                t = tags[("in", nb)] = tags.get(("in", nb), 0) + 1
-                comm.wait(nb, t, stream=st)
-                dst.copy_(comm.mailbox_view(nb, tuple(dst.shape), x.dtype, offset=(t % 2) * rb))
-                comm.ack(nb, t, stream=st)
-            else:
-                dst.zero_()
+        ops = []
+        if g > 0:  # my first row -> g-1's bottom halo; g-1's last row -> my top halo
+            ops += [(g - 1, "send", ext[1]), (g - 1, "recv", ext[0])]
+        if g < N - 1:
+            ops += [(g + 1, "send", ext[h]), (g + 1, "recv", ext[h + 1])]
+        if ops:
+            comm.p2p(ops, stream=st)
         x = conv(ext, w, b, i < len(dec.layers) - 1)
     return x

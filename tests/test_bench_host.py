@@ -1,7 +1,7 @@
 """Host logic of bench.py (no GPU): the default mesh choice (CFG first, then the largest Ulysses degree
 dividing H -- P:414), the config object both arms print, and the algorithmic
 communication bytes per rank (Table 1)."""
-import argparse
+import pytest
 
 import bench
 from paper_2411_01738_b200 import usp
@@ -21,13 +21,42 @@ def test_default_split():
 
 def test_reference_arm_prints_our_config():
     for name in ("flux", "pixart", "cogvideox"):
-        a = argparse.Namespace(gpus=8, ulysses=0, ring=0, transport="peer")
+        a = bench.parse(["--gpus", "8", "--config", name])
         cfg = bench.ours_config(a, WORKLOADS[name])
         assert cfg["workload"] == name and cfg["cfg"] * cfg["ulysses"] * cfg["ring"] == 8
-        assert cfg["transport"] == "peer"
-    a = argparse.Namespace(gpus=1, ulysses=0, ring=0, transport="peer")
+        assert cfg["data_plane"] == "nccl"
+    a = bench.parse([])
     cfg = bench.ours_config(a, WORKLOADS["flux"])
-    assert cfg["transport"] is None and cfg["l2"] == "inputs larger than L2"
+    assert cfg["data_plane"] is None and cfg["l2"] == "inputs larger than L2"
+    assert a.gpus == 1 and a.config == "flux" and a.warmup >= 3
+
+
+def test_world_size_must_match_gpus(monkeypatch):
+    """Under torchrun, WORLD_SIZE != --gpus fails loudly instead of benchmarking another N."""
+    monkeypatch.setenv("WORLD_SIZE", "2")
+    monkeypatch.setenv("RANK", "0")
+    with pytest.raises(SystemExit) as e:
+        bench.main(["--gpus", "8", "--impl", "reference"])
+    assert "WORLD_SIZE=2" in str(e.value)
+
+
+def test_gpus_without_torchrun_relaunches(monkeypatch):
+    """--gpus N (N > 1) without WORLD_SIZE re-launches under torch.distributed.run with N local ranks."""
+    monkeypatch.delenv("WORLD_SIZE", raising=False)
+    seen = {}
+    monkeypatch.setattr(bench.subprocess, "call", lambda cmd: seen.setdefault("cmd", cmd) and 0)
+    assert bench.main(["--gpus", "4", "--steps", "2"]) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert "--master-addr=127.0.0.1" in cmd and cmd[-3:] == ["--gpus", "4", "--steps", "2"][-3:]
+
+
+def test_phase_summary_bandwidth():
+    ph = {"total_ms": 2.0, "a2a_in_ms": 0.2, "a2a_out_ms": 0.1, "attn_ms": [0.8, 0.8], "ring_comm_ms": [0.5],
+          "a2a_in_bytes": 90_000_000, "a2a_out_bytes": 30_000_000, "ring_bytes": [180_000_000]}
+    s = bench.phase_summary([ph, dict(ph, a2a_in_ms=0.3)])
+    assert s["a2a_in_ms"] == 0.3 and abs(s["bandwidth"]["a2a_in"]["GBps"] - 300.0) < 1e-9
+    assert abs(s["bandwidth"]["ring"]["GBps"] - 360.0) < 1e-9 and s["bandwidth"]["ring"]["hidden_under_attention"]
 
 
 def test_comm_bytes_match_table1():

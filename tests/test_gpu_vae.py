@@ -4,7 +4,7 @@
 * the decode on one device against `oracle.vae.serial_decode`;
 * bands with halo rows (virtual devices, in one process) reproduce the one-device decode BIT FOR BIT
   -- the kernel sums every pixel in one fixed order, so patch parallelism is exact (P:427);
-* one process per band through the peer-transport mailbox: tests/test_gpu_peer.py.
+* one process per band, halos over NCCL: tests/test_gpu_multiproc.py.
 """
 import numpy as np
 import pytest

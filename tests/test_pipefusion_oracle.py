@@ -125,3 +125,50 @@ def test_stale_context_hand_derivation():
     # and it is NOT the serial result: staleness is visible
     ser, _ = serial_run(x0, W, 2, sigma)
     assert np.abs(got - ser).max() > 1e-3
+
+
+# ---- hybrid PipeFusion x SP (NEXT 3 as scoped)
+HYBRID_SPLITS = [(1, 1), (2, 1), (1, 2), (2, 2), (4, 1), (1, 4), (2, 4), (4, 2)]
+
+
+@pytest.mark.parametrize("u,r", HYBRID_SPLITS)
+def test_hybrid_equals_pure_pipefusion(u, r):
+    """SPEC S:431 "Hybrid = pure PipeFusion: for any sp_degree, hybrid latents equal pure PipeFusion
+    latents with identical (pipefusion_degree, M) within 1e-10" -- SP is exact once the SP group
+    keeps the K,V it receives, ragged shards and text with patch 0 included."""
+    x = inputs(B=2, S_txt=5, S_img=43, H=4, D=8, seed=3)
+    W = weights(3, 4, 8, 4)
+    kw = dict(T=4, M=3, warmup=1, sigma=0.3, S_txt=5)
+    want, _ = pf.pipefusion(x, W, **kw)
+    got, kv = pf.hybrid(x, W, u=u, r=r, **kw)
+    assert np.abs(got - want).max() <= 1e-10 * np.abs(want).max()
+    # "the KV involved in Attention computation on different devices within the SP group should be
+    # consistent" (P:401): ranks of one head block hold identical buffers
+    for g in range(u * r):
+        for g2 in range(g % u, u * r, u):
+            for l in range(3):
+                assert np.array_equal(kv[g][l][0], kv[g2][l][0]) and np.array_equal(kv[g][l][1], kv[g2][l][1])
+
+
+@pytest.mark.parametrize("u,r", [(2, 1), (1, 2), (2, 2)])
+def test_hybrid_naive_sp_diverges(u, r):
+    """The "standard SP" ablation ("device 0 only updates K, V belonging to the even-numbered
+    patches"; SPEC S:423): discarding the received K,V leaves buffers inconsistent and the latent wrong."""
+    x = inputs(B=1, S_txt=3, S_img=40, H=2, D=8, seed=5)
+    W = weights(2, 2, 8, 6)
+    kw = dict(T=3, M=4, warmup=1, sigma=0.3, S_txt=3)
+    want, _ = pf.pipefusion(x, W, **kw)
+    bad, kv = pf.hybrid(x, W, u=u, r=r, naive=True, **kw)
+    assert np.abs(bad - want).max() > 1e-3 * np.abs(want).max()
+    assert any(not np.array_equal(kv[0][0][0], kv[g][0][0]) for g in range(u, u * r, u)) or r == 1
+
+
+def test_hybrid_all_synchronous_is_serial():
+    """warmup = T: every step synchronous, so hybrid = the serial DiT forward."""
+    x = inputs(B=1, S_txt=4, S_img=24, H=2, D=8, seed=7)
+    W = weights(2, 2, 8, 8)
+    got, _ = pf.hybrid(x, W, T=2, M=3, warmup=2, sigma=0.4, S_txt=4, u=2, r=2)
+    want = x.copy()
+    for _ in range(2):
+        want = want - 0.4 * pf.serial_eps(want, W)
+    assert np.abs(got - want).max() <= 1e-12 * np.abs(want).max()
