@@ -428,6 +428,7 @@ def main(argv=None):
             graph_note = f"capture failed, eager: {type(ex).__name__}: {ex}"[:200]
             torch.cuda.synchronize()
             barrier()
+    g = None  # only `graph` references the captured graph (teardown order, below)
     n_captured = usp.launch_count()
     timed_step = graph.replay if graph is not None else step
     n0 = usp.launch_count()
@@ -635,6 +636,10 @@ def main(argv=None):
             line["ranks"] = ranks
             line["nccl_version"] = ".".join(str(x) for x in torch.cuda.nccl.version())
         print(json.dumps(line), flush=True)
+    # teardown: the captured graph holds NCCL operations of the library's communicators, so it goes
+    # before them (destroying a communicator a live graph still references can block), then the
+    # library's communicators, then torch's process group
+    del graph, timed_step
     torch.cuda.synchronize()
     if N > 1:
         dist.barrier()
