@@ -15,6 +15,8 @@ namespace xdit {
 namespace {
 
 constexpr int kRowsPerItem = 256;  // query rows per work item (tile pair / CTA pair)
+// floats at the end of the attention scratch holding the persistent kernel's work-unit counter
+constexpr size_t kCounterFloats = 4;
 
 struct EpiParams {
   void* o;
@@ -28,6 +30,10 @@ struct EpiParams {
   // by tail_merge_kernel -- this fills the last, partial wave of the grid.
   int n_qt, n_full, n_split, kv_chunk;
   float* part;  // [n_tail * n_split][256][D] fp32 O, then [n_tail * n_split][256] fp32 LSE
+  // Persistent CTA pairs: n_units = n_full + n_tail * n_split work units; unit_counter (zeroed
+  // before the launch, in the caller's scratch) hands them out dynamically, else round-robin.
+  int n_units;
+  unsigned* unit_counter;
   // Ring merge fused into the epilogue (a7, reading C9; CTA-pair kernel): merge = 1 combines this
   // launch's (O_s, LSE_s) row with the accumulator row (acc_o, acc_l_in; layout acc_map) by their
   // log-sum-exp; merge_final = 0 writes the result back to acc_o (in place) and acc_l_out, 1 writes

@@ -1,4 +1,4 @@
-// attn_fwd_2sm.cu -- flash-attention forward on a CTA PAIR (cta_group::2) for B200 (sm_100a).
+// attn_fwd_2sm.cu -- persistent flash-attention forward on CTA PAIRS (cta_group::2) for B200 (sm_100a).
 //
 // The bf16 attention of the hot path (§4.1.1 / P:257 §4.1.2;
 // readings C1-C3, C10, R1): O = softmax(Q K^T / sqrt(D)) V and LSE for one (Q block, KV block),
@@ -9,21 +9,33 @@
 // columns alias, so QK^T of the next key tile of a query tile cannot start before the P.V of the
 // current one -- every step of a tile is a serial chain softmax -> PV -> QK^T, and the tensor core
 // idled ~40 % (round 1's one-CTA kernel, profiles/r01_ncu_attn_flux.md; retired in round 2, in git
-// history).  Here the two SMs of a TPC run one 256-row work item together with M = 256 MMAs, which
+// history).  Here the two SMs of a TPC run one 256-row work unit together with M = 256 MMAs, which
 // frees TMEM for DOUBLE-BUFFERED S and P per SM:
-//   * CTA rank r owns query rows [128 r, 128 r + 128) of the item: its Q tile, its S/P/O in TMEM;
+//   * CTA rank r owns query rows [128 r, 128 r + 128) of the unit: its Q tile, its S/P/O in TMEM;
 //   * each CTA loads HALF of every K tile (keys [64 r, 64 r + 64)) and HALF of every V tile
 //     (head-dim columns [D/2 r, D/2 r + D/2)): the pair's MMAs read the other half from the peer SM,
 //     so L2->SM traffic per SM equals the one-CTA kernel's (two query tiles per K/V load) and the
 //     smem operand traffic per SM drops to 3/4 (QK^T) and 1/2 (PV);
-//   * the leader's MMA warp issues QK^T(j+2) into S[j%2] as soon as the softmax has loaded S(j)
-//     into registers -- before PV(j) -- so the tensor core has the next score tile queued while the
-//     softmax of step j runs; P(j) goes to P[j%2], free once PV(j-2) has completed;
+//   * the leader's MMA warp issues QK^T(g+2) into S[g%2] as soon as the softmax has loaded S(g)
+//     into registers -- before PV(g) -- so the tensor core has the next score tile queued while the
+//     softmax of step g runs; P(g) goes to P[g%2], free once PV(g-2) has completed;
 //   * 8 softmax warps per CTA, two per TMEM lane quarter, alternating key tiles (see the softmax
 //     section): one runs its exp2 stream while the other loads and reduces its S; they hand the
 //     rows' running max over through smem.
+// PERSISTENT (round 2): one CTA pair per TPC loops over work units (a unit = 256 query rows of one
+// (batch, head) against its key range), so the per-unit prologue (launch, barrier init, TMEM
+// allocation, Q load latency, pipeline fill) and the drain are paid once per pair instead of once
+// per unit (measured 5.5-6 us per unit in the non-persistent kernel, profiles/r02_sweep_items.txt --
+// 17 % of a PixArt/SD3-sized unit).  Q is double-buffered in smem, so the next unit's first two
+// QK^T run while the current unit's last P.V and epilogue drain; the first P.V of a unit waits only
+// until the previous unit's epilogue has read O out of TMEM (o_empty).  The K/V smem ring, the S/P
+// TMEM buffers and every barrier phase continue across units (global tile counter g).  Units are
+// handed out by an atomic counter in the caller's scratch (dynamic: pairs that start late -- e.g.
+// behind a concurrent NCCL kernel of the ring's side stream -- simply take fewer units) or, without
+// scratch, round-robin; the leader's TMA warp fetches each unit id and broadcasts it through a small
+// smem ring into both CTAs.
 // TMEM per SM (512 columns): S[0] [0,128) S[1] [128,256) P[0] [256,320) P[1] [320,384) O [384,384+D).
-// Head dims 128 and 64 (the V halves of D = 64 are 32 columns: 64-byte swizzled rows).
+// Head dims 128, 72 and 64 (the V halves of D = 64 are 32 columns: 64-byte swizzled rows).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -47,6 +59,7 @@ constexpr int kKeys = 128;         // keys per step
 constexpr float kRescaleThresh = 8.0f;  // log2 units
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kRegsSoftmax = 216, kRegsOther = 72;  // setmaxnreg split of 384 x 168 registers
+constexpr int kRing = 8;           // work-unit broadcast ring depth (units in flight <= 5, see below)
 // exp2 pairs (of every 8) the softmax evaluates with the FMA-pipe polynomial instead of MUFU.EX2.
 // Release builds: 0 (profiles/r01_bench_flux*.json: the polynomial draws more power in the
 // power-capped sustained run for no throughput gain).  A/B builds set it with -DXDIT_EXP_EMU=n.
@@ -89,16 +102,56 @@ struct Cfg {
   static constexpr int kNPV = 2 * kVCols;                // N of the main PV MMA
   static constexpr int kOW = kNPV + (kTail ? 32 : 0);    // O columns in TMEM
   static constexpr int kStageBytes = ((kKBytes > kVBytes ? kKBytes : kVBytes) + 1023) / 1024 * 1024;
-  static constexpr int kStages = D == 128 ? 10 : (D == 64 ? 20 : 14);  // even: K even stages, V odd
-  static constexpr int kSmemBar = 512;
-  static constexpr int kSmemBytes = ((kQBytes + 1023) / 1024 * 1024) + kStages * kStageBytes + kSmemBar + 1024;
+  // even: K in even stages, V in odd; D = 128 keeps 8 (4 key tiles) so the double-buffered Q fits
+  static constexpr int kStages = D == 128 ? 8 : (D == 64 ? 20 : 14);
+  static constexpr int kSmemBar = 1024;
   static constexpr int kQRegion = (kQBytes + 1023) / 1024 * 1024;
+  static constexpr int kSmemBytes = 2 * kQRegion + kStages * kStageBytes + kSmemBar + 1024;
+  // O columns per softmax warp in the epilogue: warp c of a lane quarter takes the 32-column chunks
+  // c, c + 2, ... (D = 72: c = 0 also takes the 8 columns 64-71)
+  static constexpr int kOChunks = ((D / 32) + 1) / 2;
   __host__ __device__ static constexpr uint32_t col_s(int b) { return uint32_t(b) * 128u; }
   __host__ __device__ static constexpr uint32_t col_p(int b) { return 256u + uint32_t(b) * 64u; }
   static constexpr uint32_t kColO = 384u;
   static_assert(kColO + kOW <= kTmemCols, "TMEM budget");
-  static_assert(kSmemBytes <= 227 * 1024, "smem budget");
+  static_assert(kSmemBytes + 6 * 1024 <= 227 * 1024, "smem budget (dynamic + static)");
 };
+
+// One work unit: 256 query rows (this CTA: 128) of one (batch, head) against a key range.
+struct Unit {
+  int valid, b, h, m0, kv0, kv_len, piece, n_kv;
+};
+
+// Units [0, n_full) are whole items (query-tile pair, head, batch; query tile fastest) over all keys;
+// each of the remaining n_tail items is split into n_split key ranges of kv_chunk keys (tail split).
+__device__ __forceinline__ Unit decode_unit(const EpiParams& p, int u, uint32_t rank) {
+  Unit U{};
+  U.valid = u >= 0;
+  if (!U.valid) return U;
+  int item = u, kv0 = 0, kv_len = p.Skv, piece = -1;
+  if (item >= p.n_full) {
+    const int r = item - p.n_full;
+    piece = r;
+    item = p.n_full + r / p.n_split;
+    kv0 = (r % p.n_split) * p.kv_chunk;
+    kv_len = min(p.kv_chunk, p.Skv - kv0);
+  }
+  const int hb = item / p.n_qt;
+  U.h = hb % p.H;
+  U.b = hb / p.H;
+  U.m0 = (item % p.n_qt) * kRowsPerItem + int(rank) * kRows;
+  U.kv0 = kv0;
+  U.kv_len = kv_len;
+  U.piece = piece;
+  U.n_kv = (kv_len + kKeys - 1) / kKeys;
+  return U;
+}
+
+// The id of this pair's t-th unit from the broadcast ring (every role of both CTAs reads it).
+__device__ __forceinline__ int ring_get(const volatile int* ring, uint64_t* full, int t) {
+  ptx::mbar_wait_acq_cluster(&full[t % kRing], (t / kRing) & 1);
+  return ring[t % kRing];
+}
 
 // Scores of keys >= valid (columns col0.. of this 32-column block) -> -inf: exp2 gives exactly 0.
 __device__ __forceinline__ void mask_tail(uint32_t (&a)[32], int col0, int valid) {
@@ -166,6 +219,40 @@ __device__ __forceinline__ float exp_pack32(const uint32_t (&a)[32], int col0, i
   return (s0 + s1) + (s2 + s3);
 }
 
+// o[i] <- wbl * o[i] + wa * acc[i] for n consecutive fp32 columns (the fused ring merge, a7)
+template <int N>
+__device__ __forceinline__ void merge_cols(uint32_t* o, const float* acc, float wbl, float wa) {
+  const float4* ap = reinterpret_cast<const float4*>(acc);
+#pragma unroll
+  for (int i = 0; i < N / 4; ++i) {
+    const float4 y = ap[i];
+    o[4 * i] = f2u(fmaf(wbl, u2f(o[4 * i]), wa * y.x));
+    o[4 * i + 1] = f2u(fmaf(wbl, u2f(o[4 * i + 1]), wa * y.y));
+    o[4 * i + 2] = f2u(fmaf(wbl, u2f(o[4 * i + 2]), wa * y.z));
+    o[4 * i + 3] = f2u(fmaf(wbl, u2f(o[4 * i + 3]), wa * y.w));
+  }
+}
+
+// store n fp32 columns scaled by sc, as fp32 or bf16
+template <int N>
+__device__ __forceinline__ void store_cols(const uint32_t* o, float sc, void* base, int64_t off, int of32) {
+  if (of32) {
+    float4* dp = reinterpret_cast<float4*>(static_cast<float*>(base) + off);
+#pragma unroll
+    for (int i = 0; i < N / 4; ++i)
+      dp[i] = make_float4(u2f(o[4 * i]) * sc, u2f(o[4 * i + 1]) * sc, u2f(o[4 * i + 2]) * sc,
+                          u2f(o[4 * i + 3]) * sc);
+  } else {
+    uint4* dp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(base) + off);
+#pragma unroll
+    for (int i = 0; i < N / 8; ++i)
+      dp[i] = make_uint4(ptx::pack_bf16x2(u2f(o[8 * i]) * sc, u2f(o[8 * i + 1]) * sc),
+                         ptx::pack_bf16x2(u2f(o[8 * i + 2]) * sc, u2f(o[8 * i + 3]) * sc),
+                         ptx::pack_bf16x2(u2f(o[8 * i + 4]) * sc, u2f(o[8 * i + 5]) * sc),
+                         ptx::pack_bf16x2(u2f(o[8 * i + 6]) * sc, u2f(o[8 * i + 7]) * sc));
+  }
+}
+
 template <int D, int EMU>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     attn_fwd_2sm_kernel(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
@@ -176,39 +263,35 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sKV = smem + C::kQRegion;
+  uint8_t* sQ = smem;  // two Q buffers of kQRegion bytes (unit parity)
+  uint8_t* sKV = smem + 2 * C::kQRegion;
   __shared__ float m_pub[2 * kRows];     // [step parity][row]: running max after that step
   __shared__ float xsum[2 * kRows];      // [warp pair half][row]: partial row sums for the epilogue
   __shared__ float xref[2 * kRows];      // [warp pair half][row]: the max those sums refer to
+  __shared__ int unit_ring[kRing];       // this pair's unit ids (written by the leader's TMA warp)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::kStageBytes);
-  uint64_t* q_full = bars;                    // leader: both Q tiles landed
-  uint64_t* kv_full = q_full + 1;             // leader: both halves of a K / V stage landed
+  uint64_t* q_full = bars;                    // leader [2]: both Q tiles of a unit landed
+  uint64_t* q_empty = q_full + 2;             // each CTA [2]: the unit's last QK^T completed
+  uint64_t* kv_full = q_empty + 2;            // leader: both halves of a K / V stage landed
   uint64_t* kv_empty = kv_full + C::kStages;  // each CTA: the pair's MMAs are done with a stage
   uint64_t* s_full = kv_empty + C::kStages;   // each CTA: S[b] written
   uint64_t* s_free = s_full + 2;              // leader: the pair's 8 softmax warps of S[b] loaded it
   uint64_t* p_full = s_free + 2;              // leader: the pair's 8 softmax warps of P[b] stored it
   uint64_t* pv_done = p_full + 2;             // each CTA: PV reading P[b] completed
-  uint64_t* o_full = pv_done + 2;             // each CTA: last PV completed
-  uint64_t* m_ready = o_full + 1;             // [lane quarter][step parity]: m_pub written
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(m_ready + 8);
+  uint64_t* o_full = pv_done + 2;             // each CTA: a unit's last PV completed
+  uint64_t* o_empty = o_full + 1;             // leader: the pair's 16 softmax warps read O out
+  uint64_t* m_ready = o_empty + 1;            // [lane quarter][step parity]: m_pub written
+  uint64_t* unit_full = m_ready + 8;          // each CTA [kRing]: unit_ring[slot] written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(unit_full + kRing);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
-  int item = blockIdx.x >> 1, kv0 = 0, kv_len = p.Skv, piece = -1;
-  if (item >= p.n_full) {  // tail item: one key range of a split (query-tile pair, head, batch)
-    const int r = item - p.n_full;
-    piece = r;
-    item = p.n_full + r / p.n_split;
-    kv0 = (r % p.n_split) * p.kv_chunk;
-    kv_len = min(p.kv_chunk, p.Skv - kv0);
-  }
-  const int hb = item / p.n_qt, h = hb % p.H, b = hb / p.H;
-  const int m0 = (item % p.n_qt) * kRowsPerItem + int(rank) * kRows;  // this CTA's first query row
-  const int n_kv = (kv_len + kKeys - 1) / kKeys;
 
   if (threadIdx.x == 0) {
-    ptx::mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&q_full[i], 1);
+      ptx::mbar_init(&q_empty[i], 1);
+    }
     for (int s = 0; s < C::kStages; ++s) {
       ptx::mbar_init(&kv_full[s], 1);
       ptx::mbar_init(&kv_empty[s], 1);
@@ -220,7 +303,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       ptx::mbar_init(&pv_done[t], 1);
     }
     ptx::mbar_init(o_full, 1);
+    ptx::mbar_init(o_empty, 16);
     for (int i = 0; i < 8; ++i) ptx::mbar_init(&m_ready[i], 32);
+    for (int i = 0; i < kRing; ++i) ptx::mbar_init(&unit_full[i], 1);
     ptx::fence_mbar_init();
   }
   if (warp == kWarpMma) {
@@ -246,39 +331,62 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
    ptx::setmaxnreg_dec<kRegsOther>();
    if (warp == kWarpTma) {
     // ===================================================== TMA producer (both CTAs)
+    // The leader's lane 0 also hands out the units: the t-th unit of this pair is fetched when the
+    // TMA warp starts it (after q_empty(t-2): every role has then read the ids of units <= t-4, so
+    // a ring of 8 slots is never overwritten while still needed) and broadcast into both CTAs.
     const uint64_t pol_q = ptx::policy_evict_first();
     const uint64_t pol_kv = ptx::policy_evict_last();
-    const uint32_t qfull_cl = ptx::mapa(q_full, 0);
-    if (ptx::elect_one()) {
-      if (rank == 0) ptx::mbar_expect_tx(q_full, 2 * C::kQBytes);
-      for (int a = 0; a < C::kN128; ++a)
-        ptx::tma_load_4d_pair(sQ + a * C::kAtom, &tmQ, qfull_cl, a * 64, h, m0, b, pol_q);
-      if (C::kTail)
-        ptx::tma_load_4d_pair(sQ + C::kN128 * C::kAtom, &tmQ16, qfull_cl, C::kN128 * 64, h, m0, b, pol_q);
-    }
-    __syncwarp();
-    for (int it = 0; it < 2 * n_kv; ++it) {
-      const int j = it >> 1, stage = it % C::kStages, round = it / C::kStages;
-      if (round > 0) ptx::mbar_wait_cluster(&kv_empty[stage], (round - 1) & 1);
-      if (ptx::elect_one()) {
-        if (rank == 0) ptx::mbar_expect_tx(&kv_full[stage], 2 * ((it & 1) ? C::kVBytes : C::kKBytes));
-        const uint32_t full_cl = ptx::mapa(&kv_full[stage], 0);
-        uint8_t* dst = sKV + stage * C::kStageBytes;
-        if ((it & 1) == 0) {  // K half: keys [64 rank, 64 rank + 64) of the tile, all D columns
-          for (int a = 0; a < C::kN128; ++a)
-            ptx::tma_load_4d_pair(dst + a * C::kKHalfAtom, &tmK, full_cl, a * 64, h,
-                                  kv0 + j * kKeys + int(rank) * 64, b, pol_kv);
-          if (C::kTail)
-            ptx::tma_load_4d_pair(dst + C::kN128 * C::kKHalfAtom, &tmK16, full_cl, C::kN128 * 64, h,
-                                  kv0 + j * kKeys + int(rank) * 64, b, pol_kv);
-        } else {  // V half: all 128 keys, head-dim columns [kVCols rank, kVCols rank + kVCols) (+ tail)
-          ptx::tma_load_4d_pair(dst, &tmV, full_cl, int(rank) * C::kVCols, h, kv0 + j * kKeys, b, pol_kv);
-          if (C::kTail)
-            ptx::tma_load_4d_pair(dst + C::kVBytesA, &tmV16, full_cl, 2 * C::kVCols + 16 * int(rank), h,
-                                  kv0 + j * kKeys, b, pol_kv);
+    const int pid = blockIdx.x >> 1, npg = gridDim.x >> 1;
+    uint32_t it = 0;  // K/V half loads issued so far (2 per key tile, across units)
+    for (int t = 0;; ++t) {
+      const int qb = t & 1;
+      if (t >= 2) ptx::mbar_wait_cluster(&q_empty[qb], ((t - 2) >> 1) & 1);
+      if (rank == 0 && lane == 0) {
+        int u = p.unit_counter ? int(atomicAdd(p.unit_counter, 1u)) : pid + t * npg;
+        if (u >= p.n_units) u = -1;
+        for (uint32_t r = 0; r < 2; ++r) {
+          ptx::st_cluster_u32(ptx::mapa(&unit_ring[t % kRing], r), uint32_t(u));
+          ptx::mbar_arrive_release_cluster(ptx::mapa(&unit_full[t % kRing], r));
         }
       }
       __syncwarp();
+      const Unit U = decode_unit(p, ring_get(unit_ring, unit_full, t), rank);
+      if (!U.valid) break;
+      uint8_t* q_dst = sQ + qb * C::kQRegion;
+      const uint32_t qfull_cl = ptx::mapa(&q_full[qb], 0);
+      if (ptx::elect_one()) {
+        if (rank == 0) ptx::mbar_expect_tx(&q_full[qb], 2 * C::kQBytes);
+        for (int a = 0; a < C::kN128; ++a)
+          ptx::tma_load_4d_pair(q_dst + a * C::kAtom, &tmQ, qfull_cl, a * 64, U.h, U.m0, U.b, pol_q);
+        if (C::kTail)
+          ptx::tma_load_4d_pair(q_dst + C::kN128 * C::kAtom, &tmQ16, qfull_cl, C::kN128 * 64, U.h, U.m0, U.b,
+                                pol_q);
+      }
+      __syncwarp();
+      for (int i = 0; i < 2 * U.n_kv; ++i, ++it) {
+        const int j = i >> 1, stage = it % C::kStages, round = it / C::kStages;
+        if (round > 0) ptx::mbar_wait_cluster(&kv_empty[stage], (round - 1) & 1);
+        if (ptx::elect_one()) {
+          if (rank == 0) ptx::mbar_expect_tx(&kv_full[stage], 2 * ((i & 1) ? C::kVBytes : C::kKBytes));
+          const uint32_t full_cl = ptx::mapa(&kv_full[stage], 0);
+          uint8_t* dst = sKV + stage * C::kStageBytes;
+          const int key0 = U.kv0 + j * kKeys;
+          if ((i & 1) == 0) {  // K half: keys [64 rank, 64 rank + 64) of the tile, all D columns
+            for (int a = 0; a < C::kN128; ++a)
+              ptx::tma_load_4d_pair(dst + a * C::kKHalfAtom, &tmK, full_cl, a * 64, U.h, key0 + int(rank) * 64,
+                                    U.b, pol_kv);
+            if (C::kTail)
+              ptx::tma_load_4d_pair(dst + C::kN128 * C::kKHalfAtom, &tmK16, full_cl, C::kN128 * 64, U.h,
+                                    key0 + int(rank) * 64, U.b, pol_kv);
+          } else {  // V half: all 128 keys, head-dim columns [kVCols rank, kVCols rank + kVCols) (+ tail)
+            ptx::tma_load_4d_pair(dst, &tmV, full_cl, int(rank) * C::kVCols, U.h, key0, U.b, pol_kv);
+            if (C::kTail)
+              ptx::tma_load_4d_pair(dst + C::kVBytesA, &tmV16, full_cl, 2 * C::kVCols + 16 * int(rank), U.h,
+                                    key0, U.b, pol_kv);
+          }
+        }
+        __syncwarp();
+      }
     }
    } else if (warp == kWarpMma) {
     // ===================================================== MMA issuer (leader CTA, one lane)
@@ -287,23 +395,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       constexpr uint32_t idesc_pv = ptx::idesc_bf16_f32(2 * kRows, C::kNPV, 0, 1);
       constexpr uint32_t idesc_pv16 = ptx::idesc_bf16_f32(2 * kRows, 32, 0, 1);
       const uint32_t sQa = ptx::smem_u32(sQ), sKVa = ptx::smem_u32(sKV);
-      auto kv_wait = [&](int idx) -> int {
+      auto kv_wait = [&](uint32_t idx) -> int {
         const int stage = idx % C::kStages;
         ptx::mbar_wait_cluster(&kv_full[stage], (idx / C::kStages) & 1);
         return stage;
       };
       // S[jb] = Q K_j^T: A = Q (K-major, 128B swizzle, atoms of 128 rows), B = the K halves
       // (K-major, atoms of 64 keys); 16-element K step k at atom k/4, byte 32 (k%4).
-      auto qk = [&](int jb, int sK) {
-        const uint32_t ka = sKVa + sK * C::kStageBytes;
+      auto qk = [&](int jb, int sK, int qb) {
+        const uint32_t ka = sKVa + sK * C::kStageBytes, qa = sQa + qb * C::kQRegion;
 #pragma unroll
         for (int k = 0; k < C::kDpK / 16; ++k) {
           if (C::kTail && k == C::kN128 * 4)  // D = 72: the 32B-swizzled tail atom is one K step
-            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc(sQa + C::kN128 * C::kAtom, 16, 8 * 32, ptx::kLayoutSW32),
+            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc(qa + C::kN128 * C::kAtom, 16, 8 * 32, ptx::kLayoutSW32),
                              ptx::sdesc(ka + C::kN128 * C::kKHalfAtom, 16, 8 * 32, ptx::kLayoutSW32), idesc_qk,
                              1u);
           else
-            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc_sw128(sQa + (k >> 2) * C::kAtom + (k & 3) * 32, 16, 1024),
+            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc_sw128(qa + (k >> 2) * C::kAtom + (k & 3) * 32, 16, 1024),
                              ptx::sdesc_sw128(ka + (k >> 2) * C::kKHalfAtom + (k & 3) * 32, 16, 1024), idesc_qk,
                              k > 0 ? 1u : 0u);
         }
@@ -322,271 +430,274 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                              (acc || k > 0) ? 1u : 0u);
         }
       };
-      ptx::mbar_wait_cluster(q_full, 0);
-      // QK^T runs two key tiles ahead of PV: S[j%2] is rewritten by QK^T(j+2) as soon as the
-      // softmax has loaded S(j) (it does so in the middle of step j-1), so the tensor core always
-      // has the next score tile queued while PV waits for the softmax.
-      auto issue_qk = [&](int jq) {
-        const int sK = kv_wait(2 * jq);
-        if (jq >= 2) ptx::mbar_wait_cluster(&s_free[jq & 1], ((jq - 2) >> 1) & 1);
+      // Two cursors over this pair's stream of key tiles (global tile counter g across units): QK^T
+      // runs two tiles ahead of PV, so S[g%2] is rewritten by QK^T(g+2) as soon as the softmax has
+      // loaded S(g) -- across a unit boundary too (the next unit's Q is already in its buffer).
+      struct Cur {
+        int t, j, n_kv, valid;
+        uint32_t g;
+      };
+      auto load = [&](Cur& c) {
+        const Unit U = decode_unit(p, ring_get(unit_ring, unit_full, c.t), 0);
+        c.valid = U.valid;
+        c.n_kv = U.valid ? U.n_kv : 0;
+        c.j = 0;
+      };
+      auto advance = [&](Cur& c) {
+        ++c.g;
+        if (++c.j == c.n_kv) {
+          ++c.t;
+          load(c);
+        }
+      };
+      auto issue_qk = [&](const Cur& c) {
+        const int qb = c.t & 1;
+        if (c.j == 0) ptx::mbar_wait_cluster(&q_full[qb], (c.t >> 1) & 1);
+        const int sK = kv_wait(2 * c.g);
+        if (c.g >= 2) ptx::mbar_wait_cluster(&s_free[c.g & 1], ((c.g - 2) >> 1) & 1);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
-          qk(jq & 1, sK);
-          ptx::tc_commit_pair(&s_full[jq & 1]);
+          qk(c.g & 1, sK, qb);
+          ptx::tc_commit_pair(&s_full[c.g & 1]);
           ptx::tc_commit_pair(&kv_empty[sK]);
+          if (c.j == c.n_kv - 1) ptx::tc_commit_pair(&q_empty[qb]);
         }
         __syncwarp();
       };
-      issue_qk(0);
-      if (n_kv > 1) issue_qk(1);
-      for (int j = 0; j < n_kv; ++j) {
-        if (j + 2 < n_kv) issue_qk(j + 2);
-        stamp(p, j, 2);
-        const int sV = kv_wait(2 * j + 1);
-        stamp(p, j, 3);
-        ptx::mbar_wait_cluster(&p_full[j & 1], (j >> 1) & 1);
-        stamp(p, j, 4);
+      Cur qc{0, 0, 0, 0, 0u}, pc{0, 0, 0, 0, 0u};
+      load(qc);
+      load(pc);
+      for (int w = 0; w < 2 && qc.valid; ++w) {
+        issue_qk(qc);
+        advance(qc);
+      }
+      while (pc.valid) {
+        if (qc.valid) {
+          issue_qk(qc);
+          advance(qc);
+        }
+        stamp(p, pc.g, 2);
+        const int sV = kv_wait(2 * pc.g + 1);
+        stamp(p, pc.g, 3);
+        ptx::mbar_wait_cluster(&p_full[pc.g & 1], (pc.g >> 1) & 1);
+        if (pc.j == 0 && pc.t > 0) ptx::mbar_wait_cluster(o_empty, (pc.t - 1) & 1);  // O read out
+        stamp(p, pc.g, 4);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
-          pv(j & 1, sV, j > 0);
-          ptx::tc_commit_pair(&pv_done[j & 1]);
+          pv(pc.g & 1, sV, pc.j > 0);
+          ptx::tc_commit_pair(&pv_done[pc.g & 1]);
           ptx::tc_commit_pair(&kv_empty[sV]);
-          if (j == n_kv - 1) ptx::tc_commit_pair(o_full);
+          if (pc.j == pc.n_kv - 1) ptx::tc_commit_pair(o_full);
         }
         __syncwarp();
-        stamp(p, j, 5);
+        stamp(p, pc.g, 5);
+        advance(pc);
       }
     }
    }
   } else {
     ptx::setmaxnreg_inc<kRegsSoftmax>();
     // ===================================================== softmax (8 warps per CTA)
-    // Warp w owns TMEM lanes / query rows 32 (w%4) .. +31 and the key tiles j = w/4 (mod 2): the two
-    // warps of a lane quarter alternate steps, so one runs its exp2 stream while the other waits
-    // for S, loads it, finds its row max and stores P -- the MUFU pipe of the SM sub-partition
-    // stays busy.  They share the rows' running max m (reading R1: it moves, rescaling O, only when
-    // the tile max exceeds it by more than 2^kRescaleThresh): the warp of step j publishes m(j) in
-    // smem (mbarrier m_ready[w%4][j%2]) right after its max pass, the warp of step j+1 reads it.
-    // Each warp keeps its own partial row sum l_w relative to the m it last used; the epilogue
-    // combines the two.
-    const int g = warp & 3, c = warp >> 2;
-    const int row_in_tile = g * 32 + lane;
-    const uint32_t lane_off = uint32_t(g * 32) << 16;
+    // Warp w owns TMEM lanes / query rows 32 (w%4) .. +31 and the key tiles g = w/4 (mod 2) of the
+    // pair's tile stream: the two warps of a lane quarter alternate steps, so one runs its exp2
+    // stream while the other waits for S, loads it, finds its row max and stores P -- the MUFU pipe
+    // of the SM sub-partition stays busy.  They share the rows' running max m (reading R1: it
+    // moves, rescaling O, only when the tile max exceeds it by more than 2^kRescaleThresh): the warp
+    // of step g publishes m(g) in smem (mbarrier m_ready[w%4][g%2]) right after its max pass, the
+    // warp of step g+1 of the same unit reads it.  Each warp keeps its own partial row sum l_w
+    // relative to the m it last used; the unit's epilogue combines the two.
+    const int g4 = warp & 3, c = warp >> 2;
+    const int row_in_tile = g4 * 32 + lane;
+    const uint32_t lane_off = uint32_t(g4 * 32) << 16;
     const float sl2 = p.scale_log2;
     const uint32_t s_free_cl = ptx::mapa(&s_free[c], 0);  // the leader's barriers for S[c] / P[c]
     const uint32_t p_full_cl = ptx::mapa(&p_full[c], 0);
+    const uint32_t o_empty_cl = ptx::mapa(o_empty, 0);
     const uint32_t tO = tmem + lane_off + C::kColO;
-    float m_ref = -INFINITY, l = 0.f, m_used = 0.f;
-    for (int j = c; j < n_kv; j += 2) {
-      ptx::mbar_wait_cluster(&s_full[c], (j >> 1) & 1);
-      ptx::tc_fence_after();
+    uint32_t gbase = 0;  // global index of the unit's first key tile
+    for (int t = 0;; ++t) {
+      const int uid = ring_get(unit_ring, unit_full, t);
+      if (uid < 0) break;
+      int kv_len, n_kv;  // only these stay live through the tile loop; the rest is decoded after it
+      {
+        const Unit U = decode_unit(p, uid, rank);
+        kv_len = U.kv_len;
+        n_kv = U.n_kv;
+      }
+      float m_ref = -INFINITY, l = 0.f, m_used = 0.f;
+      for (int j = int((gbase ^ uint32_t(c)) & 1u); j < n_kv; j += 2) {
+        const uint32_t g = gbase + uint32_t(j);
+        ptx::mbar_wait_cluster(&s_full[c], (g >> 1) & 1);
+        ptx::tc_fence_after();
 #ifdef XDIT_PROFILE
-      if (p.diag) {  // profiling builds only: hand the barriers back without softmax work
+        if (p.diag) {  // profiling builds only: hand the barriers back without softmax work
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);
+          if (g >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((g - 2) >> 1) & 1);
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive_cluster(p_full_cl);
+          if (j > 0) ptx::mbar_wait(&m_ready[g4 * 2 + ((g - 1) & 1)], ((g - 1) >> 1) & 1);
+          m_pub[(g & 1) * kRows + row_in_tile] = 0.f;
+          ptx::mbar_arrive(&m_ready[g4 * 2 + (g & 1)]);
+          l = 1.f;
+          m_ref = m_used = 0.f;
+          continue;
+        }
+#endif
+        uint32_t s0[32], s1[32], s2[32], s3[32];
+        const uint32_t tS = tmem + lane_off + C::col_s(c);
+        ptx::tmem_ld32(tS, s0);
+        ptx::tmem_ld32(tS + 32, s1);
+        ptx::tmem_ld32(tS + 64, s2);
+        ptx::tmem_ld32(tS + 96, s3);
+        ptx::tmem_ld_wait();
+        ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);
-        if (j >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((j - 2) >> 1) & 1);
+        if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);  // S[c] may be rewritten by QK^T(g+2)
+        const int valid = kv_len - j * kKeys;  // keys of this tile that exist (C16)
+        if (valid < kKeys) {  // ragged last tile: missing keys get score -inf (weight 0), once, here --
+          // the max and exp code below then has no per-element mask (with the masked variants as
+          // separate template instances the compiler if-converted them into every tile's exp loop)
+          mask_tail(s0, 0, valid);
+          mask_tail(s1, 32, valid);
+          mask_tail(s2, 64, valid);
+          mask_tail(s3, 96, valid);
+        }
+        const float m_tile = fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2;
+        if (j == 0) {
+          m_used = m_tile;
+        } else {
+          ptx::mbar_wait(&m_ready[g4 * 2 + ((g - 1) & 1)], ((g - 1) >> 1) & 1);
+          const float m_prev = m_pub[((g - 1) & 1) * kRows + row_in_tile];
+          const bool up = m_tile > m_prev + kRescaleThresh;
+          m_used = up ? m_tile : m_prev;
+          if (__any_sync(0xffffffffu, up)) {  // rare: O *= 2^(m_prev - m_used) once PV(g-1) is in
+            const float alpha = ptx::ex2(m_prev - m_used);
+            ptx::mbar_wait_cluster(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            ptx::tc_fence_after();
+#pragma unroll
+            for (int cc = 0; cc < (D / 32) * 32; cc += 32) {
+              uint32_t o[32];
+              ptx::tmem_ld32(tO + cc, o);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+              ptx::tmem_st32(tO + cc, o);
+            }
+            if (D % 32) {  // D = 72: columns 64-71 (72-95 hold zeros)
+              uint32_t o[8];
+              ptx::tmem_ld8(tO + (D / 32) * 32, o);
+              ptx::tmem_ld_wait();
+#pragma unroll
+              for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+              ptx::tmem_st8(tO + (D / 32) * 32, o);
+            }
+            ptx::tmem_st_wait();
+          }
+        }
+        m_pub[(g & 1) * kRows + row_in_tile] = m_used;
+        ptx::mbar_arrive(&m_ready[g4 * 2 + (g & 1)]);  // all 32 lanes (count 32)
+        if (m_used != m_ref) {
+          l *= ptx::ex2(m_ref - m_used);  // 0 * 0 on this warp's first step of the unit
+          m_ref = m_used;
+        }
+        uint32_t pk[32];
+        float rs;
+        rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_used, pk);
+        rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_used, pk + 16);
+        if (g >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((g - 2) >> 1) & 1);  // P[c] free again
+        ptx::tc_fence_after();
+        const uint32_t tP = tmem + lane_off + C::col_p(c);
+        ptx::tmem_st32(tP, pk);  // keys 0..63
+        rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_used, pk);
+        rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_used, pk + 16);
+        ptx::tmem_st32(tP + 32, pk);  // keys 64..127
+        l += rs;
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(p_full_cl);
-        if (j + 1 < n_kv) {  // keep the running-max hand-over in step
-          if (j > 0) ptx::mbar_wait(&m_ready[g * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-          m_pub[(j & 1) * kRows + row_in_tile] = 0.f;
-          ptx::mbar_arrive(&m_ready[g * 2 + (j & 1)]);
-        }
-        l = 1.f;
-        m_ref = m_used = 0.f;
-        continue;
       }
-#endif
-      uint32_t s0[32], s1[32], s2[32], s3[32];
-      const uint32_t tS = tmem + lane_off + C::col_s(c);
-      ptx::tmem_ld32(tS, s0);
-      ptx::tmem_ld32(tS + 32, s1);
-      ptx::tmem_ld32(tS + 64, s2);
-      ptx::tmem_ld32(tS + 96, s3);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);  // S[c] may be rewritten by QK^T(j+2)
-      const int valid = kv_len - j * kKeys;  // keys of this tile that exist (C16)
-      if (valid < kKeys) {  // ragged last tile: missing keys get score -inf (weight 0), once, here --
-        // the max and exp code below then has no per-element mask (with the masked variants as
-        // separate template instances the compiler if-converted them into every tile's exp loop)
-        mask_tail(s0, 0, valid);
-        mask_tail(s1, 32, valid);
-        mask_tail(s2, 64, valid);
-        mask_tail(s3, 96, valid);
-      }
-      const float m_tile = fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2;
-      if (j == 0) {
-        m_used = m_tile;
-      } else {
-        ptx::mbar_wait(&m_ready[g * 2 + ((j - 1) & 1)], ((j - 1) >> 1) & 1);
-        const float m_prev = m_pub[((j - 1) & 1) * kRows + row_in_tile];
-        const bool up = m_tile > m_prev + kRescaleThresh;
-        m_used = up ? m_tile : m_prev;
-        if (__any_sync(0xffffffffu, up)) {  // rare: O *= 2^(m_prev - m_used) once PV(j-1) is in
-          const float alpha = ptx::ex2(m_prev - m_used);
-          ptx::mbar_wait_cluster(&pv_done[(j - 1) & 1], ((j - 1) >> 1) & 1);
-          ptx::tc_fence_after();
-#pragma unroll
-          for (int cc = 0; cc < (D / 32) * 32; cc += 32) {
-            uint32_t o[32];
-            ptx::tmem_ld32(tO + cc, o);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
-            ptx::tmem_st32(tO + cc, o);
-          }
-          if (D % 32) {  // D = 72: columns 64-71 (72-95 hold zeros)
-            uint32_t o[8];
-            ptx::tmem_ld8(tO + (D / 32) * 32, o);
-            ptx::tmem_ld_wait();
-#pragma unroll
-            for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
-            ptx::tmem_st8(tO + (D / 32) * 32, o);
-          }
-          ptx::tmem_st_wait();
-        }
-      }
-      m_pub[(j & 1) * kRows + row_in_tile] = m_used;
-      ptx::mbar_arrive(&m_ready[g * 2 + (j & 1)]);  // all 32 lanes (count 32)
-      if (m_used != m_ref) {
-        l *= ptx::ex2(m_ref - m_used);  // 0 * 0 on this warp's first step
-        m_ref = m_used;
-      }
-      uint32_t pk[32];
-      float rs;
-      rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_used, pk);
-      rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_used, pk + 16);
-      if (j >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((j - 2) >> 1) & 1);  // P[c] free again
+      // ----------------------------------------------- the unit's epilogue: O / l, LSE
+      // final m = m of the unit's last step; l = sum over both warps of l_w 2^(m_ref_w - m)
+      const Unit U = decode_unit(p, uid, rank);
+      const uint32_t glast = gbase + uint32_t(n_kv) - 1u;
+      xsum[c * kRows + row_in_tile] = l;
+      xref[c * kRows + row_in_tile] = m_ref;
+      ptx::named_bar_sync(1 + g4, 64);
+      m_used = m_pub[(glast & 1) * kRows + row_in_tile];
+      l = xsum[row_in_tile] * ptx::ex2(xref[row_in_tile] - m_used) +
+          xsum[kRows + row_in_tile] * ptx::ex2(xref[kRows + row_in_tile] - m_used);
+      ptx::named_bar_sync(1 + g4, 64);  // xsum / xref / m_pub read: the next unit may rewrite them
+      // O out of TMEM into registers, then hand TMEM's O to the next unit's first P.V
+      ptx::mbar_wait_cluster(o_full, t & 1);
       ptx::tc_fence_after();
-      const uint32_t tP = tmem + lane_off + C::col_p(c);
-      ptx::tmem_st32(tP, pk);  // keys 0..63
-      rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_used, pk);
-      rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_used, pk + 16);
-      ptx::tmem_st32(tP + 32, pk);  // keys 64..127
-      l += rs;
-      ptx::tmem_st_wait();
+      uint32_t o[C::kOChunks][32];
+      uint32_t o8[8];
+#pragma unroll
+      for (int k = 0; k < C::kOChunks; ++k)
+        if (c * 32 + 64 * k < (D / 32) * 32) ptx::tmem_ld32(tO + c * 32 + 64 * k, o[k]);
+      if (D % 32 && c == 0) ptx::tmem_ld8(tO + (D / 32) * 32, o8);
+      ptx::tmem_ld_wait();
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive_cluster(p_full_cl);
-    }
-    // ------------------------------------------------- epilogue: O / l, LSE
-    // final m = m of the last step; l = sum over both warps of l_w 2^(m_ref_w - m)
-    xsum[c * kRows + row_in_tile] = l;
-    xref[c * kRows + row_in_tile] = m_ref;
-    ptx::named_bar_sync(1 + g, 64);
-    m_used = m_pub[((n_kv - 1) & 1) * kRows + row_in_tile];
-    l = xsum[row_in_tile] * ptx::ex2(xref[row_in_tile] - m_used) +
-        xsum[kRows + row_in_tile] * ptx::ex2(xref[kRows + row_in_tile] - m_used);
-    ptx::mbar_wait_cluster(o_full, 0);
-    ptx::tc_fence_after();
-    const int row = m0 + row_in_tile;
-    const float inv_l = 1.f / l;
-    RowDst dst = rowmap_dst(p.map, b, row, h);
-    void* obase = p.o;
-    float* lbase = p.lse;
-    int of32 = p.out_f32;
-    float lse_row = (m_used + log2f(l)) * 0.69314718055994530942f;
-    // fused ring merge (a7): O = wa * O_acc + wb * O_s, LSE by log-sum-exp (lse_merge_kernel's
-    // arithmetic); wb folds in 1/l.  Results go back to the accumulator or, at the last ring step,
-    // to the final destination.
-    const bool mrg = p.merge && piece < 0 && row < p.Sq;
-    float wa = 0.f, wbl = inv_l;
-    RowDst ad{0, 0};
-    if (mrg) {
-      ad = rowmap_dst(p.acc_map, b, row, h);
-      const float la = p.acc_l_in[ad.l_off];
-      const float M2 = fmaxf(la, lse_row);
-      const float L2 = M2 + logf(expf(la - M2) + expf(lse_row - M2));
-      wa = expf(la - L2);
-      wbl = expf(lse_row - L2) * inv_l;
-      lse_row = L2;
-      if (!p.merge_final) {
-        obase = p.acc_o;
-        lbase = p.acc_l_out;
-        of32 = 1;
-        dst = ad;
-      }
-    }
-    if (piece >= 0) {  // split tail item: normalised fp32 partial for tail_merge_kernel
-      const int64_t prow = int64_t(piece) * kRowsPerItem + int(rank) * kRows + row_in_tile;
-      const int64_t n_pieces = int64_t(gridDim.x >> 1) - p.n_full;
-      obase = p.part;
-      lbase = p.part + n_pieces * kRowsPerItem * D;
-      of32 = 1;
-      dst.o_off = prow * D;
-      dst.l_off = prow;
-    }
-    const bool valid_row = row < p.Sq;
-#pragma unroll
-    for (int col = c * 32; col < (D / 32) * 32; col += 64) {  // this warp's 32-column chunks of O
-      uint32_t o[32];
-      ptx::tmem_ld32(tO + col, o);
-      ptx::tmem_ld_wait();
-      if (mrg) {  // o <- wa * acc + wb * O_s, then stored with inv_l = 1
-        const float4* ap = reinterpret_cast<const float4*>(p.acc_o + ad.o_off + col);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const float4 y = ap[i];
-          o[4 * i] = f2u(fmaf(wbl, u2f(o[4 * i]), wa * y.x));
-          o[4 * i + 1] = f2u(fmaf(wbl, u2f(o[4 * i + 1]), wa * y.y));
-          o[4 * i + 2] = f2u(fmaf(wbl, u2f(o[4 * i + 2]), wa * y.z));
-          o[4 * i + 3] = f2u(fmaf(wbl, u2f(o[4 * i + 3]), wa * y.w));
-        }
-      }
-      const float sc = mrg ? 1.f : inv_l;
-      if (valid_row) {
-        if (of32) {
-          float4* dp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + col);
-#pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dp[i] = make_float4(u2f(o[4 * i]) * sc, u2f(o[4 * i + 1]) * sc, u2f(o[4 * i + 2]) * sc,
-                                u2f(o[4 * i + 3]) * sc);
-        } else {
-          uint4* dp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + col);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dp[i] = make_uint4(ptx::pack_bf16x2(u2f(o[8 * i]) * sc, u2f(o[8 * i + 1]) * sc),
-                               ptx::pack_bf16x2(u2f(o[8 * i + 2]) * sc, u2f(o[8 * i + 3]) * sc),
-                               ptx::pack_bf16x2(u2f(o[8 * i + 4]) * sc, u2f(o[8 * i + 5]) * sc),
-                               ptx::pack_bf16x2(u2f(o[8 * i + 6]) * sc, u2f(o[8 * i + 7]) * sc));
-        }
-      }
-    }
-    if (D % 32 && c == 0) {  // D = 72: columns 64-71
-      constexpr int col = (D / 32) * 32;
-      uint32_t o[8];
-      ptx::tmem_ld8(tO + col, o);
-      ptx::tmem_ld_wait();
+      if (lane == 0) ptx::mbar_arrive_cluster(o_empty_cl);
+      const int row = U.m0 + row_in_tile;
+      const float inv_l = 1.f / l;
+      RowDst dst = rowmap_dst(p.map, U.b, row, U.h);
+      void* obase = p.o;
+      float* lbase = p.lse;
+      int of32 = p.out_f32;
+      float lse_row = (m_used + log2f(l)) * 0.69314718055994530942f;
+      // fused ring merge (a7): O = wa * O_acc + wb * O_s, LSE by log-sum-exp (lse_merge_kernel's
+      // arithmetic); wb folds in 1/l.  Results go back to the accumulator or, at the last ring step,
+      // to the final destination.
+      const bool mrg = p.merge && U.piece < 0 && row < p.Sq;
+      float wa = 0.f, wbl = inv_l;
+      RowDst ad{0, 0};
       if (mrg) {
-        const float4* ap = reinterpret_cast<const float4*>(p.acc_o + ad.o_off + col);
-#pragma unroll
-        for (int i = 0; i < 2; ++i) {
-          const float4 y = ap[i];
-          o[4 * i] = f2u(fmaf(wbl, u2f(o[4 * i]), wa * y.x));
-          o[4 * i + 1] = f2u(fmaf(wbl, u2f(o[4 * i + 1]), wa * y.y));
-          o[4 * i + 2] = f2u(fmaf(wbl, u2f(o[4 * i + 2]), wa * y.z));
-          o[4 * i + 3] = f2u(fmaf(wbl, u2f(o[4 * i + 3]), wa * y.w));
+        ad = rowmap_dst(p.acc_map, U.b, row, U.h);
+        const float la = p.acc_l_in[ad.l_off];
+        const float M2 = fmaxf(la, lse_row);
+        const float L2 = M2 + logf(expf(la - M2) + expf(lse_row - M2));
+        wa = expf(la - L2);
+        wbl = expf(lse_row - L2) * inv_l;
+        lse_row = L2;
+        if (!p.merge_final) {
+          obase = p.acc_o;
+          lbase = p.acc_l_out;
+          of32 = 1;
+          dst = ad;
         }
       }
+      if (U.piece >= 0) {  // split tail unit: normalised fp32 partial for tail_merge_kernel
+        const int64_t prow = int64_t(U.piece) * kRowsPerItem + int(rank) * kRows + row_in_tile;
+        const int64_t n_pieces = int64_t(p.n_units) - p.n_full;
+        obase = p.part;
+        lbase = p.part + n_pieces * kRowsPerItem * D;
+        of32 = 1;
+        dst.o_off = prow * D;
+        dst.l_off = prow;
+      }
+      const bool valid_row = row < p.Sq;
       const float sc = mrg ? 1.f : inv_l;
-      if (valid_row) {
-        if (of32) {
-          float4* dp = reinterpret_cast<float4*>(static_cast<float*>(obase) + dst.o_off + col);
-          dp[0] = make_float4(u2f(o[0]) * sc, u2f(o[1]) * sc, u2f(o[2]) * sc, u2f(o[3]) * sc);
-          dp[1] = make_float4(u2f(o[4]) * sc, u2f(o[5]) * sc, u2f(o[6]) * sc, u2f(o[7]) * sc);
-        } else {
-          uint4* dp = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(obase) + dst.o_off + col);
-          dp[0] = make_uint4(ptx::pack_bf16x2(u2f(o[0]) * sc, u2f(o[1]) * sc),
-                             ptx::pack_bf16x2(u2f(o[2]) * sc, u2f(o[3]) * sc),
-                             ptx::pack_bf16x2(u2f(o[4]) * sc, u2f(o[5]) * sc),
-                             ptx::pack_bf16x2(u2f(o[6]) * sc, u2f(o[7]) * sc));
+#pragma unroll
+      for (int k = 0; k < C::kOChunks; ++k) {  // this warp's 32-column chunks of O
+        const int col = c * 32 + 64 * k;
+        if (col < (D / 32) * 32) {
+          if (mrg) merge_cols<32>(o[k], p.acc_o + ad.o_off + col, wbl, wa);  // then stored with sc = 1
+          if (valid_row) store_cols<32>(o[k], sc, obase, dst.o_off + col, of32);
         }
       }
+      if (D % 32 && c == 0) {  // D = 72: columns 64-71
+        constexpr int col = (D / 32) * 32;
+        if (mrg) merge_cols<8>(o8, p.acc_o + ad.o_off + col, wbl, wa);
+        if (valid_row) store_cols<8>(o8, sc, obase, dst.o_off + col, of32);
+      }
+      if (c == 0 && valid_row && lbase)
+        lbase[dst.l_off] = U.piece >= 0 ? (m_used + log2f(l)) * 0.69314718055994530942f : lse_row;
+      gbase += uint32_t(n_kv);
     }
-    if (c == 0 && valid_row && lbase) lbase[dst.l_off] = piece >= 0 ? (m_used + log2f(l)) * 0.69314718055994530942f
-                                                                 : lse_row;
   }
   __syncwarp();
   ptx::tc_fence_before();
@@ -642,9 +753,9 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.acc_l_out = a.acc_l_out;
   p.acc_map = a.acc_map;
   p.scale_log2 = float(1.4426950408889634 / std::sqrt(double(D)));
-  // Work items (256 query rows of one (batch, head)) run one per CTA pair; when the items leave a
-  // partial last wave of pairs, its items are split over key ranges written as normalised fp32
-  // partials into the scratch and merged by tail_merge_kernel (DESIGN.md §7.1 "tail split").
+  // Work units (256 query rows of one (batch, head)); when the items leave a partial last round of
+  // pairs, its items are split over key ranges written as normalised fp32 partials into the scratch
+  // and merged by tail_merge_kernel (DESIGN.md §7.1 "tail split").
   p.n_qt = (a.Sq + kRowsPerItem - 1) / kRowsPerItem;
   const int items = p.n_qt * a.H * a.B;
   p.n_full = items;
@@ -653,6 +764,8 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   p.part = nullptr;
   int n_tail = 0;
   const int npairs = device_sm_count() / 2;
+  // the last kCounterFloats floats of the scratch hold the unit counter (dynamic unit hand-out)
+  const size_t part_floats = a.scratch_floats > kCounterFloats ? a.scratch_floats - kCounterFloats : 0;
   if (a.scratch && items > npairs && items % npairs) {
     const int rem = items % npairs, n_kv_tiles = (a.Skv + kKeys - 1) / kKeys;
     int ns = std::min(std::min(npairs / rem, 8), n_kv_tiles / 2);
@@ -660,7 +773,7 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
       const int chunk = ((n_kv_tiles + ns - 1) / ns) * kKeys;
       ns = (a.Skv + chunk - 1) / chunk;
       const size_t need = size_t(rem) * ns * kRowsPerItem * (D + 1);
-      if (ns >= 2 && need <= a.scratch_floats) {
+      if (ns >= 2 && need <= part_floats) {
         n_tail = rem;
         p.n_full = items - rem;
         p.n_split = ns;
@@ -669,7 +782,14 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
       }
     }
   }
-  const dim3 grid(2 * (p.n_full + n_tail * p.n_split));
+  p.n_units = p.n_full + n_tail * p.n_split;
+  p.unit_counter = nullptr;
+  if (a.scratch && a.scratch_floats >= kCounterFloats) {
+    p.unit_counter = reinterpret_cast<unsigned*>(a.scratch + a.scratch_floats - kCounterFloats);
+    cudaError_t e = cudaMemsetAsync(p.unit_counter, 0, sizeof(unsigned), st);
+    if (e != cudaSuccess) return e;
+  }
+  const dim3 grid(2 * std::min(p.n_units, npairs));
 #ifdef XDIT_PROFILE
   // profiling builds: XDIT_PROFILE_DIAG=1 in the environment runs the softmax-free skeleton,
   // XDIT_PROFILE_TRACE=1 prints the first pair's clock64 stamps after the launch
@@ -718,7 +838,9 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
 }  // namespace pair2
 }  // namespace
 
-size_t attn_scratch_floats(int D) { return size_t(device_sm_count()) * kRowsPerItem * size_t(D + 1); }
+size_t attn_scratch_floats(int D) {
+  return size_t(device_sm_count()) * kRowsPerItem * size_t(D + 1) + kCounterFloats;
+}
 
 bool attn_fused_merge_supported(int D) { return D == 128 || D == 64 || D == 72; }
 

@@ -152,3 +152,46 @@ def test_attn_tail_split_vs_oracle(D, Skv):
     got_o = o[:, rows.cuda()][:, :, heads]
     got_l = l[:, heads][:, :, rows.cuda()]
     assert_bf16(errors(got_o, got_l, ref_o, ref_l))
+
+
+@pytest.mark.parametrize("D", [64, 72, 128])
+@pytest.mark.parametrize("Skv", [100, 300, 777])
+@pytest.mark.parametrize("dynamic", [False, True])
+def test_attn_persistent_many_units_vs_oracle(D, Skv, dynamic):
+    """The persistent CTA pairs run several work units each (B=2, H=40, Sq=600: 240 units on 74
+    pairs), with 1, 3 and 7 key tiles per unit (odd and even counts flip which softmax warp of a
+    lane quarter starts the next unit) and a ragged last query tile; units handed out round-robin
+    (no scratch) or by the scratch's atomic counter (dynamic, which also enables the tail split)."""
+    B, H, Sq = 2, 40, 600
+    q, _, _ = qkv(B, Sq, H, D, seed=700 + D + Skv)
+    _, k, v = qkv(B, Skv, H, D, seed=800 + D + Skv)
+    o = torch.empty(q.shape, dtype=torch.bfloat16, device="cuda")
+    l = torch.empty((B, H, Sq), dtype=torch.float32, device="cuda")
+    scratch = torch.empty(usp.attn_scratch_bytes(D) // 4, dtype=torch.float32, device="cuda") if dynamic else None
+    for _ in range(2):  # the second launch re-zeroes the unit counter
+        usp.attn_fwd(q.cuda(), k.cuda(), v.cuda(), o, l, B=B, H=H, Sq=Sq, Skv=Skv, D=D,
+                     q_strides=(Sq * H * D, H * D, D), kv_strides=(Skv * H * D, H * D, D),
+                     omap=usp.RowMap.plain(B, Sq, H, D), scratch=scratch)
+    torch.cuda.synchronize()
+    heads = [0, 17, 39]
+    ref_o, ref_l = oracle.attention(f64(q[:, :, heads]), f64(k[:, :, heads]), f64(v[:, :, heads]))
+    assert_bf16(errors(o[:, :, heads], l[:, heads], ref_o, ref_l))
+    # every head has been written (a unit lost by the hand-out would leave garbage rows)
+    assert torch.isfinite(o.float()).all() and torch.isfinite(l).all()
+
+
+def test_attn_persistent_deterministic_across_handout():
+    """Dynamic hand-out changes which pair runs a unit, never its arithmetic: the output is
+    bitwise identical with and without the counter when no tail split applies (items % 74 == 0)."""
+    B, H, Sq, D = 1, 37, 512, 128  # 2 x 37 = 74 items: no partial round, no tail split
+    q, k, v = (t.cuda() for t in qkv(B, Sq, H, D, seed=4242))
+    outs = []
+    for dyn in (False, True):
+        o = torch.empty(q.shape, dtype=torch.bfloat16, device="cuda")
+        l = torch.empty((B, H, Sq), dtype=torch.float32, device="cuda")
+        scratch = torch.empty(usp.attn_scratch_bytes(D) // 4, dtype=torch.float32, device="cuda") if dyn else None
+        usp.attn_fwd(q, k, v, o, l, B=B, H=H, Sq=Sq, Skv=Sq, D=D, q_strides=(Sq * H * D, H * D, D),
+                     kv_strides=(Sq * H * D, H * D, D), omap=usp.RowMap.plain(B, Sq, H, D), scratch=scratch)
+        torch.cuda.synchronize()
+        outs.append((o, l))
+    assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
