@@ -78,12 +78,12 @@ __device__ __forceinline__ uint64_t add2(uint64_t a, uint64_t b) {
 // j = round(x) (magic-number add), f in [-0.5, 0.5]; 2^f by a degree-4 polynomial with p(0) = 1
 // exactly (minimax on [-0.5, 0.5], max relative error 2.9e-6, mean 3e-7 -- far below the bf16
 // rounding P gets anyway, and no bias on the row sum l); 2^j is added straight into the exponent
-// field.  x is clamped at -125 so the result stays a normal number.
+// field.  x is clamped to [-125, 127] so the result stays a normal number.
 __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
   float x0, x1;
   up2(x2, x0, x1);
-  x0 = fmaxf(x0, -125.f);
-  x1 = fmaxf(x1, -125.f);
+  x0 = fminf(fmaxf(x0, -125.f), 127.f);  // 2^127 still flags the softmax's overflow test
+  x1 = fminf(fmaxf(x1, -125.f), 127.f);
   const uint64_t xc = pk2(x0, x1);
   const uint64_t magic = pk2(12582912.f, 12582912.f), nmagic = pk2(-12582912.f, -12582912.f);
   const uint64_t t = add2(xc, magic);             // 1.5*2^23 + round(x)

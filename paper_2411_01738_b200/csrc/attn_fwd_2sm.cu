@@ -20,12 +20,13 @@
 //     into registers -- before PV(g) -- so the tensor core has the next score tile queued while the
 //     softmax of step g runs; P(g) goes to P[g%2], free once PV(g-2) has completed;
 //   * 8 softmax warps per CTA, two per TMEM lane quarter, alternating key tiles (see the softmax
-//     section): one runs its exp2 stream while the other loads and reduces its S; they hand the
-//     rows' running max over through smem.
+//     section): one runs its exp2 stream while the other loads its S; P is computed against a
+//     reference max without a max pass and reconciled with the other warp's reference at the end of
+//     the step (reading R1').
 // PERSISTENT (round 2): one CTA pair per TPC loops over work units (a unit = 256 query rows of one
 // (batch, head) against its key range), so the per-unit prologue (launch, barrier init, TMEM
 // allocation, Q load latency, pipeline fill) and the drain are paid once per pair instead of once
-// per unit (measured 5.5-6 us per unit in the non-persistent kernel, profiles/r02_sweep_items.txt --
+// per unit (measured 5.5-6 us per unit in the non-persistent kernel, profiles/r02_sweep_items_nonpersistent.txt --
 // 17 % of a PixArt/SD3-sized unit).  Q is double-buffered in smem, so the next unit's first two
 // QK^T run while the current unit's last P.V and epilogue drain; the first P.V of a unit waits only
 // until the previous unit's epilogue has read O out of TMEM (o_empty).  The K/V smem ring, the S/P
@@ -54,27 +55,30 @@ namespace pair2 {
 
 constexpr int kThreads = 384;      // 8 softmax warps, TMA warp, MMA warp, 2 idle warps
 constexpr int kWarpTma = 8, kWarpMma = 9;
+
 constexpr int kRows = 128;         // query rows per CTA (= TMEM lanes)
 constexpr int kKeys = 128;         // keys per step
-constexpr float kRescaleThresh = 8.0f;  // log2 units
+constexpr float kMoveThresh = 40.0f;    // log2 units: a reference jump above 2^40 moves it (R1')
 constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kRegsSoftmax = 216, kRegsOther = 72;  // setmaxnreg split of 384 x 168 registers
 constexpr int kRing = 8;           // work-unit broadcast ring depth (units in flight <= 5, see below)
-// exp2 pairs (of every 8) the softmax evaluates with the FMA-pipe polynomial instead of MUFU.EX2.
-// Release builds: 0 (profiles/r01_bench_flux*.json: the polynomial draws more power in the
-// power-capped sustained run for no throughput gain).  A/B builds set it with -DXDIT_EXP_EMU=n.
+// exp2 pairs (of every 8) the softmax evaluates with the FMA-pipe polynomial instead of MUFU.EX2:
+// 1 (same-session A/B with the deferred reconciliation, profiles/r02_ab_softmax.txt: +1-4 % over 0
+// at every head dim, 2 is slower).  A/B builds set it with -DXDIT_EXP_EMU=n.
 #ifndef XDIT_EXP_EMU
-#define XDIT_EXP_EMU 0
+#define XDIT_EXP_EMU 1
 #endif
 #ifdef XDIT_PROFILE
-constexpr int kTraceIters = 64, kTraceEv = 16;
+constexpr int kTraceIters = 96, kTraceEv = 8, kTraceWarps = 10;
 #endif
-// Profiling builds only (-DXDIT_PROFILE, tools/ab_attn.sh): clock64 stamps of warp 0 / the MMA lane
-// of the first CTA pair (XDIT_PROFILE_TRACE) and the softmax-free skeleton (XDIT_PROFILE_DIAG).
-__device__ __forceinline__ void stamp(const EpiParams& p, int j, int ev) {
+// Profiling builds only (-DXDIT_PROFILE, tools/trace_attn.py): clock64 stamps of every warp role of
+// the first CTA pair per global key tile g (XDIT_PROFILE_TRACE=<file>: raw dump after the launch)
+// and the softmax-free skeleton (XDIT_PROFILE_DIAG=1).
+__device__ __forceinline__ void stamp(const EpiParams& p, uint32_t g, int ev) {
 #ifdef XDIT_PROFILE
-  if (p.trace && j < kTraceIters && blockIdx.x < 2 && (threadIdx.x & 31) == 0)
-    p.trace[(blockIdx.x * kTraceIters + j) * kTraceEv + ev] = clock64();
+  const int warp = threadIdx.x >> 5;
+  if (p.trace && g < uint32_t(kTraceIters) && blockIdx.x < 2 && (threadIdx.x & 31) == 0 && warp < kTraceWarps)
+    p.trace[((blockIdx.x * kTraceWarps + warp) * kTraceIters + g) * kTraceEv + ev] = clock64();
 #endif
 }
 
@@ -153,6 +157,11 @@ __device__ __forceinline__ int ring_get(const volatile int* ring, uint64_t* full
   return ring[t % kRing];
 }
 
+// Barrier waits of the single-purpose warps (TMA producer, MMA issuer): with a suspend-time hint,
+// so the warp sleeps until the phase completes instead of re-polling (A/B: +0.5-2 %,
+// profiles/r02_ab_softmax.txt; the softmax warps poll -- sleeping there cost 2-4 %).
+__device__ __forceinline__ void role_wait(uint64_t* bar, uint32_t parity) { ptx::mbar_wait_sleep(bar, parity); }
+
 // Scores of keys >= valid (columns col0.. of this 32-column block) -> -inf: exp2 gives exactly 0.
 __device__ __forceinline__ void mask_tail(uint32_t (&a)[32], int col0, int valid) {
 #pragma unroll
@@ -217,6 +226,36 @@ __device__ __forceinline__ float exp_pack32(const uint32_t (&a)[32], int col0, i
   up2(acc0, s0, s1);
   up2(acc1, s2, s3);
   return (s0 + s1) + (s2 + s3);
+}
+
+// O (this lane's row, all D columns in TMEM) *= alpha -- the rare running-max move
+template <int D>
+__device__ __forceinline__ void scale_o(uint32_t tO, float alpha) {
+#pragma unroll
+  for (int cc = 0; cc < (D / 32) * 32; cc += 32) {
+    uint32_t o[32];
+    ptx::tmem_ld32(tO + cc, o);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+    ptx::tmem_st32(tO + cc, o);
+  }
+  if (D % 32) {  // D = 72: columns 64-71 (72-95 hold zeros)
+    uint32_t o[8];
+    ptx::tmem_ld8(tO + (D / 32) * 32, o);
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
+    ptx::tmem_st8(tO + (D / 32) * 32, o);
+  }
+  ptx::tmem_st_wait();
+}
+
+// 32 packed bf16 pairs *= s (s an exact power of two: exact unless the result leaves the range)
+__device__ __forceinline__ void scale_bf16x2(uint32_t (&v)[32], float s) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    v[i] = ptx::pack_bf16x2(u2f(v[i] << 16) * s, u2f(v[i] & 0xffff0000u) * s);
 }
 
 // o[i] <- wbl * o[i] + wa * acc[i] for n consecutive fp32 columns (the fused ring merge, a7)
@@ -340,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     uint32_t it = 0;  // K/V half loads issued so far (2 per key tile, across units)
     for (int t = 0;; ++t) {
       const int qb = t & 1;
-      if (t >= 2) ptx::mbar_wait_cluster(&q_empty[qb], ((t - 2) >> 1) & 1);
+      if (t >= 2) role_wait(&q_empty[qb], ((t - 2) >> 1) & 1);
       if (rank == 0 && lane == 0) {
         int u = p.unit_counter ? int(atomicAdd(p.unit_counter, 1u)) : pid + t * npg;
         if (u >= p.n_units) u = -1;
@@ -365,7 +404,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       __syncwarp();
       for (int i = 0; i < 2 * U.n_kv; ++i, ++it) {
         const int j = i >> 1, stage = it % C::kStages, round = it / C::kStages;
-        if (round > 0) ptx::mbar_wait_cluster(&kv_empty[stage], (round - 1) & 1);
+        if (round > 0) role_wait(&kv_empty[stage], (round - 1) & 1);
+        stamp(p, it >> 1, (i & 1) ? 1 : 0);
         if (ptx::elect_one()) {
           if (rank == 0) ptx::mbar_expect_tx(&kv_full[stage], 2 * ((i & 1) ? C::kVBytes : C::kKBytes));
           const uint32_t full_cl = ptx::mapa(&kv_full[stage], 0);
@@ -397,7 +437,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       const uint32_t sQa = ptx::smem_u32(sQ), sKVa = ptx::smem_u32(sKV);
       auto kv_wait = [&](uint32_t idx) -> int {
         const int stage = idx % C::kStages;
-        ptx::mbar_wait_cluster(&kv_full[stage], (idx / C::kStages) & 1);
+        role_wait(&kv_full[stage], (idx / C::kStages) & 1);
         return stage;
       };
       // S[jb] = Q K_j^T: A = Q (K-major, 128B swizzle, atoms of 128 rows), B = the K halves
@@ -452,9 +492,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       auto issue_qk = [&](const Cur& c) {
         const int qb = c.t & 1;
-        if (c.j == 0) ptx::mbar_wait_cluster(&q_full[qb], (c.t >> 1) & 1);
+        stamp(p, c.g, 0);
+        if (c.j == 0) role_wait(&q_full[qb], (c.t >> 1) & 1);
         const int sK = kv_wait(2 * c.g);
-        if (c.g >= 2) ptx::mbar_wait_cluster(&s_free[c.g & 1], ((c.g - 2) >> 1) & 1);
+        stamp(p, c.g, 1);
+        if (c.g >= 2) role_wait(&s_free[c.g & 1], ((c.g - 2) >> 1) & 1);
+        stamp(p, c.g, 2);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
           qk(c.g & 1, sK, qb);
@@ -463,35 +506,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           if (c.j == c.n_kv - 1) ptx::tc_commit_pair(&q_empty[qb]);
         }
         __syncwarp();
+        stamp(p, c.g, 3);
       };
       Cur qc{0, 0, 0, 0, 0u}, pc{0, 0, 0, 0, 0u};
-      load(qc);
-      load(pc);
-      for (int w = 0; w < 2 && qc.valid; ++w) {
-        issue_qk(qc);
-        advance(qc);
-      }
-      while (pc.valid) {
-        if (qc.valid) {
+      auto issue_pv = [&](const Cur& c) {
+        stamp(p, c.g, 4);
+        const int sV = kv_wait(2 * c.g + 1);
+        stamp(p, c.g, 5);
+        role_wait(&p_full[c.g & 1], (c.g >> 1) & 1);
+        if (c.j == 0 && c.t > 0) role_wait(o_empty, (c.t - 1) & 1);  // O read out
+        stamp(p, c.g, 6);
+        ptx::tc_fence_after();
+        if (ptx::elect_one()) {
+          pv(c.g & 1, sV, c.j > 0);
+          ptx::tc_commit_pair(&pv_done[c.g & 1]);
+          ptx::tc_commit_pair(&kv_empty[sV]);
+          if (c.j == c.n_kv - 1) ptx::tc_commit_pair(o_full);
+        }
+        __syncwarp();
+        stamp(p, c.g, 7);
+      };
+      {
+        load(qc);
+        load(pc);
+        for (int w = 0; w < 2 && qc.valid; ++w) {
           issue_qk(qc);
           advance(qc);
         }
-        stamp(p, pc.g, 2);
-        const int sV = kv_wait(2 * pc.g + 1);
-        stamp(p, pc.g, 3);
-        ptx::mbar_wait_cluster(&p_full[pc.g & 1], (pc.g >> 1) & 1);
-        if (pc.j == 0 && pc.t > 0) ptx::mbar_wait_cluster(o_empty, (pc.t - 1) & 1);  // O read out
-        stamp(p, pc.g, 4);
-        ptx::tc_fence_after();
-        if (ptx::elect_one()) {
-          pv(pc.g & 1, sV, pc.j > 0);
-          ptx::tc_commit_pair(&pv_done[pc.g & 1]);
-          ptx::tc_commit_pair(&kv_empty[sV]);
-          if (pc.j == pc.n_kv - 1) ptx::tc_commit_pair(o_full);
+        while (pc.valid) {
+          if (qc.valid) {
+            issue_qk(qc);
+            advance(qc);
+          }
+          issue_pv(pc);
+          advance(pc);
         }
-        __syncwarp();
-        stamp(p, pc.g, 5);
-        advance(pc);
       }
     }
    }
@@ -500,12 +549,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     // ===================================================== softmax (8 warps per CTA)
     // Warp w owns TMEM lanes / query rows 32 (w%4) .. +31 and the key tiles g = w/4 (mod 2) of the
     // pair's tile stream: the two warps of a lane quarter alternate steps, so one runs its exp2
-    // stream while the other waits for S, loads it, finds its row max and stores P -- the MUFU pipe
-    // of the SM sub-partition stays busy.  They share the rows' running max m (reading R1: it
-    // moves, rescaling O, only when the tile max exceeds it by more than 2^kRescaleThresh): the warp
-    // of step g publishes m(g) in smem (mbarrier m_ready[w%4][g%2]) right after its max pass, the
-    // warp of step g+1 of the same unit reads it.  Each warp keeps its own partial row sum l_w
-    // relative to the m it last used; the unit's epilogue combines the two.
+    // stream while the other waits for S, loads it and stores P -- the MUFU pipe of the SM
+    // sub-partition stays busy.  They share the rows' reference max (reading R1', below): the warp
+    // of step g publishes the reference m(g) of its P in smem (mbarrier m_ready[w%4][g%2]) at the
+    // END of its step, the warp of step g+1 of the same unit reconciles with it before releasing
+    // P(g+1).  Each warp keeps its own partial row sum l_w relative to the reference it last used;
+    // the unit's epilogue combines the two.
     const int g4 = warp & 3, c = warp >> 2;
     const int row_in_tile = g4 * 32 + lane;
     const uint32_t lane_off = uint32_t(g4 * 32) << 16;
@@ -524,10 +573,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         kv_len = U.kv_len;
         n_kv = U.n_kv;
       }
-      float m_ref = -INFINITY, l = 0.f, m_used = 0.f;
+      float m_ref = -INFINITY, l = 0.f, m_used = 0.f, m_own = 0.f;
       for (int j = int((gbase ^ uint32_t(c)) & 1u); j < n_kv; j += 2) {
         const uint32_t g = gbase + uint32_t(j);
         ptx::mbar_wait_cluster(&s_full[c], (g >> 1) & 1);
+        stamp(p, g, 0);
         ptx::tc_fence_after();
 #ifdef XDIT_PROFILE
         if (p.diag) {  // profiling builds only: hand the barriers back without softmax work
@@ -551,6 +601,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         ptx::tmem_ld32(tS + 64, s2);
         ptx::tmem_ld32(tS + 96, s3);
         ptx::tmem_ld_wait();
+        stamp(p, g, 1);
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(s_free_cl);  // S[c] may be rewritten by QK^T(g+2)
@@ -563,60 +614,80 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
           mask_tail(s2, 64, valid);
           mask_tail(s3, 96, valid);
         }
-        const float m_tile = fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2;
-        if (j == 0) {
-          m_used = m_tile;
-        } else {
+        // Reading R1': P(g) is computed straight against a candidate reference m_c
+        // -- the tile's own max rounded up to an integer (log2 units) on the unit's first two tiles,
+        // else this warp's reference of its previous tile -- so no max pass and no hand-over sits
+        // before the exp2 stream.  The row sum flags the rare tile whose P could overflow (sum >
+        // 2^64): it is redone against its own max.  Before releasing P(g) the warp reconciles with
+        // the reference m(g-1) the other warp published at the END of step g-1 (normally long
+        // done): P(g) and its sum are scaled by the exact power of two 2^(m_c - m(g-1)) and m(g) =
+        // m(g-1); only a jump above 2^kMoveThresh moves the reference (O rescaled after PV(g-1)).
+        float m_c;
+        if (j <= 1) m_c = ceilf(fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2);
+        else m_c = m_own;
+        stamp(p, g, 2);
+        uint32_t pk[32];
+        const uint32_t tP = tmem + lane_off + C::col_p(c);
+        auto exp2x = [&](const uint32_t (&a)[32], int col0, uint32_t* pko) -> float {
+          return exp_pack32<false, EMU>(a, col0, valid, sl2, -m_c, pko);
+        };
+        float rs = exp2x(s0, 0, pk);
+        rs += exp2x(s1, 32, pk + 16);
+        stamp(p, g, 4);
+        if (g >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((g - 2) >> 1) & 1);  // P[c] free again
+        stamp(p, g, 5);
+        ptx::tc_fence_after();
+        ptx::tmem_st32(tP, pk);  // keys 0..63
+        rs += exp2x(s2, 64, pk);
+        rs += exp2x(s3, 96, pk + 16);
+        if (__any_sync(0xffffffffu, !(rs <= 0x1p64f))) {  // rare (also catches inf / NaN): own max
+          m_c = fmaxf(m_c, ceilf(fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2));
+          rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_c, pk);
+          rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_c, pk + 16);
+          ptx::tmem_st32(tP, pk);
+          rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_c, pk);
+          rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_c, pk + 16);
+        }
+        float m_fin = m_c;
+        if (j >= 1) {
           ptx::mbar_wait(&m_ready[g4 * 2 + ((g - 1) & 1)], ((g - 1) >> 1) & 1);
+          stamp(p, g, 3);
           const float m_prev = m_pub[((g - 1) & 1) * kRows + row_in_tile];
-          const bool up = m_tile > m_prev + kRescaleThresh;
-          m_used = up ? m_tile : m_prev;
-          if (__any_sync(0xffffffffu, up)) {  // rare: O *= 2^(m_prev - m_used) once PV(g-1) is in
-            const float alpha = ptx::ex2(m_prev - m_used);
-            ptx::mbar_wait_cluster(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
-            ptx::tc_fence_after();
-#pragma unroll
-            for (int cc = 0; cc < (D / 32) * 32; cc += 32) {
-              uint32_t o[32];
-              ptx::tmem_ld32(tO + cc, o);
-              ptx::tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 32; ++i) o[i] = f2u(u2f(o[i]) * alpha);
-              ptx::tmem_st32(tO + cc, o);
+          const float d = m_c - m_prev;
+          const bool move = d > kMoveThresh;
+          m_fin = move ? m_c : m_prev;
+          if (__any_sync(0xffffffffu, d != 0.f)) {  // unit's second tile, or after a rare move
+            if (__any_sync(0xffffffffu, move)) {  // O *= 2^(m_prev - m_c) once PV(g-1) is in
+              const float alpha = move ? ldexpf(1.f, int(m_prev - m_c)) : 1.f;
+              ptx::mbar_wait_cluster(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+              ptx::tc_fence_after();
+              scale_o<D>(tO, alpha);
             }
-            if (D % 32) {  // D = 72: columns 64-71 (72-95 hold zeros)
-              uint32_t o[8];
-              ptx::tmem_ld8(tO + (D / 32) * 32, o);
-              ptx::tmem_ld_wait();
-#pragma unroll
-              for (int i = 0; i < 8; ++i) o[i] = f2u(u2f(o[i]) * alpha);
-              ptx::tmem_st8(tO + (D / 32) * 32, o);
-            }
-            ptx::tmem_st_wait();
+            const float beta = move ? 1.f : ldexpf(1.f, int(d));  // exact (flushes below 2^-149)
+            uint32_t q[32];
+            ptx::tmem_st_wait();  // the first half's store has landed before it is read back
+            ptx::tmem_ld32(tP, q);
+            ptx::tmem_ld_wait();
+            scale_bf16x2(q, beta);
+            ptx::tmem_st32(tP, q);
+            scale_bf16x2(pk, beta);
+            rs *= beta;
           }
         }
-        m_pub[(g & 1) * kRows + row_in_tile] = m_used;
+        m_pub[(g & 1) * kRows + row_in_tile] = m_fin;
         ptx::mbar_arrive(&m_ready[g4 * 2 + (g & 1)]);  // all 32 lanes (count 32)
-        if (m_used != m_ref) {
-          l *= ptx::ex2(m_ref - m_used);  // 0 * 0 on this warp's first step of the unit
-          m_ref = m_used;
-        }
-        uint32_t pk[32];
-        float rs;
-        rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_used, pk);
-        rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_used, pk + 16);
-        if (g >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((g - 2) >> 1) & 1);  // P[c] free again
-        ptx::tc_fence_after();
-        const uint32_t tP = tmem + lane_off + C::col_p(c);
-        ptx::tmem_st32(tP, pk);  // keys 0..63
-        rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_used, pk);
-        rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_used, pk + 16);
         ptx::tmem_st32(tP + 32, pk);  // keys 64..127
+        if (m_fin != m_ref) {
+          l *= ptx::ex2(m_ref - m_fin);  // 0 * 0 on this warp's first step of the unit
+          m_ref = m_fin;
+        }
         l += rs;
+        m_own = m_fin;
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
         if (lane == 0) ptx::mbar_arrive_cluster(p_full_cl);
+        stamp(p, g, 6);
       }
       // ----------------------------------------------- the unit's epilogue: O / l, LSE
       // final m = m of the unit's last step; l = sum over both warps of l_w 2^(m_ref_w - m)
@@ -792,19 +863,21 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
   const dim3 grid(2 * std::min(p.n_units, npairs));
 #ifdef XDIT_PROFILE
   // profiling builds: XDIT_PROFILE_DIAG=1 in the environment runs the softmax-free skeleton,
-  // XDIT_PROFILE_TRACE=1 prints the first pair's clock64 stamps after the launch
+  // XDIT_PROFILE_TRACE=<file> appends the first pair's clock64 stamps to <file> after the launch
   static const int diag = [] {
     const char* e = std::getenv("XDIT_PROFILE_DIAG");
     return e ? std::atoi(e) : 0;
   }();
   p.diag = diag;
+  static const char* trace_file = std::getenv("XDIT_PROFILE_TRACE");
+  constexpr size_t kTraceN = size_t(2) * kTraceWarps * kTraceIters * kTraceEv;
   static unsigned long long* trace = [] {
     unsigned long long* t = nullptr;
-    if (std::getenv("XDIT_PROFILE_TRACE")) cudaMalloc(&t, sizeof(unsigned long long) * 2 * kTraceIters * kTraceEv);
+    if (trace_file) cudaMalloc(&t, sizeof(unsigned long long) * kTraceN);
     return t;
   }();
   p.trace = trace;
-  if (trace) cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * 2 * kTraceIters * kTraceEv, st);
+  if (trace) cudaMemsetAsync(trace, 0, sizeof(unsigned long long) * kTraceN, st);
 #endif
   cudaError_t err = launch_kernel<D, XDIT_EXP_EMU>(grid, m, p, st);
   if (err == cudaSuccess && n_tail) {
@@ -815,21 +888,14 @@ cudaError_t launch_d(const AttnArgs& a, cudaStream_t st) {
     err = cudaGetLastError();
   }
 #ifdef XDIT_PROFILE
-  if (trace) {  // stamps of the first pair relative to the leader's first stamp
-    static unsigned long long h[2 * kTraceIters * kTraceEv];
+  if (trace) {  // raw stamps [cta][warp][g][ev] of the first pair, appended to the trace file
+    static unsigned long long h[kTraceN];
     cudaStreamSynchronize(st);
     cudaMemcpy(h, trace, sizeof h, cudaMemcpyDeviceToHost);
-    const unsigned long long t0 = h[6];
-    fprintf(stderr, "cta j | kK sfree vwait vK pfull pvdone | e0 e1 ldiss e2 pvd st+land parr decide\n");
-    for (int cta = 0; cta < 2; ++cta)
-      for (int j = 0; j < kTraceIters; ++j) {
-        fprintf(stderr, "%d %d", cta, j);
-        for (int e = 0; e < 14; ++e) {
-          const unsigned long long v = h[(cta * kTraceIters + j) * kTraceEv + e];
-          fprintf(stderr, " %lld", v ? (long long)(v - t0) : -1LL);
-        }
-        fprintf(stderr, "\n");
-      }
+    if (FILE* f = std::fopen(trace_file, "ab")) {
+      std::fwrite(h, sizeof h, 1, f);
+      std::fclose(f);
+    }
   }
 #endif
   return err;

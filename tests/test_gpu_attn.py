@@ -195,3 +195,27 @@ def test_attn_persistent_deterministic_across_handout():
         torch.cuda.synchronize()
         outs.append((o, l))
     assert torch.equal(outs[0][0], outs[1][0]) and torch.equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("D", [64, 72, 128])
+@pytest.mark.parametrize("pattern", ["jump_up", "jump_down", "climb"])
+def test_attn_reference_max_paths_vs_oracle(D, pattern):
+    """Reading R1' (deferred reconciliation of the running max): key tiles whose scores jump far
+    above the unit's reference (x20: the exp2 row sum overflows 2^64, the tile is redone against its
+    own max and the reference moves, rescaling O), far below it (later P underflow), or climb
+    steadily (references reconciled by exact powers of two every tile)."""
+    B, H, Sq, Skv = 1, 2, 300, 1500
+    g = torch.Generator().manual_seed(31 + D)
+    q = torch.randn(B, Sq, H, D, generator=g) * 3.0
+    k = torch.randn(B, Skv, H, D, generator=g)
+    v = torch.randn(B, Skv, H, D, generator=g)
+    if pattern == "jump_up":
+        k[:, 384:] *= 20.0
+    elif pattern == "jump_down":
+        k[:, :256] *= 20.0
+    else:
+        k *= torch.linspace(1.0, 12.0, Skv).view(1, Skv, 1, 1)
+    q, k, v = (t.to(torch.bfloat16) for t in (q, k, v))
+    ref_o, ref_l = oracle.attention(f64(q), f64(k), f64(v))
+    o, l = run_attn(q.cuda(), k.cuda(), v.cuda())
+    assert_bf16(errors(o, l, ref_o, ref_l), scaled=True)  # peaky rows: |O*| up to max|V|

@@ -1,0 +1,11 @@
+timeout 300 python -m pytest tests/test_gpu_attn.py -x -q 2>&1 | tail -3
+for t in splitemu1; do XDIT_LIB=paper_2411_01738_b200/libxdit_usp_$t.so timeout 300 python -m pytest tests/test_gpu_attn.py -x -q 2>&1 | tail -2; done
+for args in "--B 1 --H 24 --S 66048 --D 128 --iters 4" "--B 1 --H 48 --S 17776 --D 64 --iters 8" \
+            "--B 2 --H 16 --S 4096 --D 72 --iters 30" "--B 2 --H 24 --S 4429 --D 64 --iters 30"; do
+  echo "== $args"
+  bash tools/ab_attn.sh "$args" dm0 base split emu1 splitemu1
+done
+for args in "--S 17776 --H 48 --D 64" "--S 66048 --H 24 --D 128"; do
+  XDIT_LIB=paper_2411_01738_b200/libxdit_usp_prof.so timeout 120 python tools/trace_attn.py $args; echo
+  XDIT_LIB=paper_2411_01738_b200/libxdit_usp_profsplitemu1.so timeout 120 python tools/trace_attn.py $args; echo
+done

@@ -1,0 +1,6 @@
+for args in "--B 1 --H 24 --S 66048 --D 128 --iters 4" "--B 1 --H 48 --S 17776 --D 64 --iters 8" \
+            "--B 2 --H 16 --S 4096 --D 72 --iters 30" "--B 2 --H 24 --S 4429 --D 64 --iters 30"; do
+  echo "== $args"
+  bash tools/ab_attn.sh "$args" base sleep1 sleep2 dm0emu1 emu2
+done
+XDIT_LIB=paper_2411_01738_b200/libxdit_usp_profsleep1.so timeout 120 python tools/trace_attn.py --S 17776 --H 48 --D 64
