@@ -457,7 +457,15 @@ def main(argv=None):
     phases = phase_summary(phs) if N > 1 else None
     pl = usp.plan(B, w.H, w.S_txt, w.S_img, w.D, u, r, sp_rank)
     kern_flops = sum(4.0 * B * pl.Hh * pl.S_blk * pl.ring_rows[s] * w.D for s in range(r))
-    kern_ms = max_over_ranks(attn_ms)
+    kern_ms = prof_kern_ms = max_over_ranks(attn_ms)
+    kern_timing = ("per-phase CUDA events of profiled calls after the timed region (xdit_comm_profile): the "
+                   "attention launches of every ring step on the caller's stream, mean over the calls")
+    if N == 1:
+        # at N = 1 a step is the attention kernel itself (plus the 4-byte reset of its unit counter):
+        # the dominant kernel's duration is the timed region's own per-step device time
+        kern_ms = ms
+        kern_timing = ("CUDA events on the launching stream around the timed steps; at N = 1 a step is one "
+                       "attention launch (+ a 4-byte cudaMemsetAsync of its unit counter)")
 
     # ---- parity of the benched run + the cpu_baseline leg (rank 0: a sample of ITS rows / heads)
     cpu, parity = None, None
@@ -622,8 +630,7 @@ def main(argv=None):
                          "frac_of_sustained": kern_tflops / peak_sus,
                          "frac_of_datasheet": kern_tflops / DATASHEET_BF16_TFLOPS,
                          "kernel_ms": kern_ms, "kernel_flops": kern_flops,
-                         "timing": "per-phase CUDA events of the benched calls (xdit_comm_profile): the attention "
-                                   "launches of every ring step on the caller's stream, mean of the profiled calls",
+                         "timing": kern_timing, "profiled_kernel_ms": prof_kern_ms,
                          "shape": f"B={B} H={pl.Hh} Sq={pl.S_blk} Skv={[pl.ring_rows[s] for s in range(r)]} D={w.D}"},
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
