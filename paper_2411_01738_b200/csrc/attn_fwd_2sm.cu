@@ -151,10 +151,17 @@ __device__ __forceinline__ Unit decode_unit(const EpiParams& p, int u, uint32_t 
   return U;
 }
 
-// The id of this pair's t-th unit from the broadcast ring (every role of both CTAs reads it).
-__device__ __forceinline__ int ring_get(const volatile int* ring, uint64_t* full, int t) {
-  ptx::mbar_wait_acq_cluster(&full[t % kRing], (t / kRing) & 1);
-  return ring[t % kRing];
+// The id of this pair's t-th unit from the broadcast ring (every role of both CTAs reads it): the
+// leader's TMA lane stores it in the LEADER's smem and arrives on both CTAs' unit_full[slot]; leader
+// roles read it locally, the peer's through distributed shared memory after a cluster-scope acquire.
+__device__ __forceinline__ int ring_get(const int* ring, uint64_t* full, int t, uint32_t rank) {
+  const int slot = t % kRing;
+  if (rank == 0) {
+    ptx::mbar_wait(&full[slot], (t / kRing) & 1);
+    return *reinterpret_cast<const volatile int*>(&ring[slot]);
+  }
+  ptx::mbar_wait_acq_cluster(&full[slot], (t / kRing) & 1);
+  return int(ptx::ld_cluster_u32(ptx::mapa(&ring[slot], 0)));
 }
 
 // Barrier waits of the single-purpose warps (TMA producer, MMA issuer): with a suspend-time hint,
@@ -307,7 +314,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   __shared__ float m_pub[2 * kRows];     // [step parity][row]: running max after that step
   __shared__ float xsum[2 * kRows];      // [warp pair half][row]: partial row sums for the epilogue
   __shared__ float xref[2 * kRows];      // [warp pair half][row]: the max those sums refer to
-  __shared__ int unit_ring[kRing];       // this pair's unit ids (written by the leader's TMA warp)
+  __shared__ int unit_ring[kRing];       // leader: this pair's unit ids (written by its TMA warp)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sKV + C::kStages * C::kStageBytes);
   uint64_t* q_full = bars;                    // leader [2]: both Q tiles of a unit landed
   uint64_t* q_empty = q_full + 2;             // each CTA [2]: the unit's last QK^T completed
@@ -383,13 +390,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (rank == 0 && lane == 0) {
         int u = p.unit_counter ? int(atomicAdd(p.unit_counter, 1u)) : pid + t * npg;
         if (u >= p.n_units) u = -1;
-        for (uint32_t r = 0; r < 2; ++r) {
-          ptx::st_cluster_u32(ptx::mapa(&unit_ring[t % kRing], r), uint32_t(u));
-          ptx::mbar_arrive_release_cluster(ptx::mapa(&unit_full[t % kRing], r));
-        }
+        *reinterpret_cast<volatile int*>(&unit_ring[t % kRing]) = u;
+        ptx::mbar_arrive(&unit_full[t % kRing]);
+        ptx::mbar_arrive_release_cluster(ptx::mapa(&unit_full[t % kRing], 1));
       }
       __syncwarp();
-      const Unit U = decode_unit(p, ring_get(unit_ring, unit_full, t), rank);
+      const Unit U = decode_unit(p, ring_get(unit_ring, unit_full, t, rank), rank);
       if (!U.valid) break;
       uint8_t* q_dst = sQ + qb * C::kQRegion;
       const uint32_t qfull_cl = ptx::mapa(&q_full[qb], 0);
@@ -478,7 +484,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t g;
       };
       auto load = [&](Cur& c) {
-        const Unit U = decode_unit(p, ring_get(unit_ring, unit_full, c.t), 0);
+        const Unit U = decode_unit(p, ring_get(unit_ring, unit_full, c.t, 0), 0);
         c.valid = U.valid;
         c.n_kv = U.valid ? U.n_kv : 0;
         c.j = 0;
@@ -565,7 +571,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     const uint32_t tO = tmem + lane_off + C::kColO;
     uint32_t gbase = 0;  // global index of the unit's first key tile
     for (int t = 0;; ++t) {
-      const int uid = ring_get(unit_ring, unit_full, t);
+      const int uid = ring_get(unit_ring, unit_full, t, rank);
       if (uid < 0) break;
       int kv_len, n_kv;  // only these stay live through the tile loop; the rest is decoded after it
       {

@@ -238,12 +238,14 @@ __device__ __forceinline__ uint32_t mapa(const void* p, uint32_t rank) {
 __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cl_addr) {
   asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
 }
-// Store a 32-bit value into a CTA's shared memory by its shared::cluster address, then arrive on
-// that CTA's mbarrier with .release.cluster semantics, so a waiter that acquires at cluster scope
-// (mbar_wait_acq_cluster) sees the value -- the persistent kernel's work-unit broadcast (once per
-// unit, off the per-tile critical path).
-__device__ __forceinline__ void st_cluster_u32(uint32_t cl_addr, uint32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(cl_addr), "r"(v) : "memory");
+// Read a 32-bit value from a CTA's shared memory by its shared::cluster address (distributed shared
+// memory), and arrive on a CTA's mbarrier with .release.cluster semantics so that a waiter acquiring
+// at cluster scope (mbar_wait_acq_cluster) sees the releasing thread's prior stores -- the
+// persistent kernel's work-unit hand-out (once per unit, off the per-tile critical path).
+__device__ __forceinline__ uint32_t ld_cluster_u32(uint32_t cl_addr) {
+  uint32_t v;
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(cl_addr) : "memory");
+  return v;
 }
 __device__ __forceinline__ void mbar_arrive_release_cluster(uint32_t cl_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cl_addr) : "memory");
