@@ -448,32 +448,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       };
       // S[jb] = Q K_j^T: A = Q (K-major, 128B swizzle, atoms of 128 rows), B = the K halves
       // (K-major, atoms of 64 keys); 16-element K step k at atom k/4, byte 32 (k%4).
+      // descriptors built once: a K step / stage / Q buffer adds its byte offset >> 4 to the start
+      // address field (bits [0,14); smem offsets stay below 2^18, so no carry leaves the field)
+      const uint64_t dq0 = ptx::sdesc_sw128(sQa, 16, 1024), dk0 = ptx::sdesc_sw128(sKVa, 16, 1024);
+      const uint64_t dq16 = ptx::sdesc(sQa + C::kN128 * C::kAtom, 16, 8 * 32, ptx::kLayoutSW32);
+      const uint64_t dk16 = ptx::sdesc(sKVa + C::kN128 * C::kKHalfAtom, 16, 8 * 32, ptx::kLayoutSW32);
+      const uint64_t dv0 = ptx::sdesc(sKVa, C::kAtom, 8 * C::kVRowBytes, C::kVLayout);
+      const uint64_t dv16 = ptx::sdesc(sKVa + C::kVBytesA, 16, 8 * 32, ptx::kLayoutSW32);
       auto qk = [&](int jb, int sK, int qb) {
-        const uint32_t ka = sKVa + sK * C::kStageBytes, qa = sQa + qb * C::kQRegion;
+        const uint64_t oq = uint64_t(uint32_t(qb * C::kQRegion) >> 4), ok = uint64_t(uint32_t(sK * C::kStageBytes) >> 4);
 #pragma unroll
         for (int k = 0; k < C::kDpK / 16; ++k) {
-          if (C::kTail && k == C::kN128 * 4)  // D = 72: the 32B-swizzled tail atom is one K step
-            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc(qa + C::kN128 * C::kAtom, 16, 8 * 32, ptx::kLayoutSW32),
-                             ptx::sdesc(ka + C::kN128 * C::kKHalfAtom, 16, 8 * 32, ptx::kLayoutSW32), idesc_qk,
-                             1u);
+          if (C::kTail && k == C::kN128 * 4)
+            ptx::mma_ss_pair(tmem + C::col_s(jb), dq16 + oq, dk16 + ok, idesc_qk, 1u);
           else
-            ptx::mma_ss_pair(tmem + C::col_s(jb), ptx::sdesc_sw128(qa + (k >> 2) * C::kAtom + (k & 3) * 32, 16, 1024),
-                             ptx::sdesc_sw128(ka + (k >> 2) * C::kKHalfAtom + (k & 3) * 32, 16, 1024), idesc_qk,
+            ptx::mma_ss_pair(tmem + C::col_s(jb), dq0 + oq + uint64_t(((k >> 2) * C::kAtom + (k & 3) * 32) >> 4),
+                             dk0 + ok + uint64_t(((k >> 2) * C::kKHalfAtom + (k & 3) * 32) >> 4), idesc_qk,
                              k > 0 ? 1u : 0u);
         }
       };
-      // O += P[jb] V_j: A = P from TMEM, B = the V halves (MN-major: 16-key step k at row 16k).
       auto pv = [&](int jb, int sV, bool acc) {
-        const uint32_t va = sKVa + sV * C::kStageBytes;
+        const uint64_t ov = uint64_t(uint32_t(sV * C::kStageBytes) >> 4);
 #pragma unroll
         for (int k = 0; k < kKeys / 16; ++k) {
           ptx::mma_ts_pair(tmem + C::kColO, tmem + C::col_p(jb) + k * 8,
-                           ptx::sdesc(va + k * 16 * C::kVRowBytes, C::kAtom, 8 * C::kVRowBytes, C::kVLayout),
-                           idesc_pv, (acc || k > 0) ? 1u : 0u);
-          if (C::kTail)  // D = 72: O columns 64-95 from the 16-column tail atoms of both CTAs
+                           dv0 + ov + uint64_t((k * 16 * C::kVRowBytes) >> 4), idesc_pv, (acc || k > 0) ? 1u : 0u);
+          if (C::kTail)
             ptx::mma_ts_pair(tmem + C::kColO + C::kNPV, tmem + C::col_p(jb) + k * 8,
-                             ptx::sdesc(va + C::kVBytesA + k * 16 * 32, 16, 8 * 32, ptx::kLayoutSW32), idesc_pv16,
-                             (acc || k > 0) ? 1u : 0u);
+                             dv16 + ov + uint64_t((k * 16 * 32) >> 4), idesc_pv16, (acc || k > 0) ? 1u : 0u);
         }
       };
       // Two cursors over this pair's stream of key tiles (global tile counter g across units): QK^T
