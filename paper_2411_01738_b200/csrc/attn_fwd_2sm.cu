@@ -634,6 +634,60 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (j <= 1) m_c = ceilf(fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2);
         else m_c = m_own;
         stamp(p, g, 2);
+        // D = 128: the whole row of P stays in registers until the end of the step: one wait for
+        // P[c] to be free (PV(g-2) done) right before both halves are stored, and the rare rescales
+        // run in registers (same-session A/B: Flux +1.5-2 %; at D = 64 / 72 it costs 3-8 %, there the
+        // first half goes out mid-step, profiles/r02_ab_p_late.txt)
+        if constexpr (D == 128) {
+        uint32_t pa[32], pb[32];
+        const uint32_t tP = tmem + lane_off + C::col_p(c);
+        float rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_c, pa);
+        rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_c, pa + 16);
+        stamp(p, g, 4);
+        rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_c, pb);
+        rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_c, pb + 16);
+        if (__any_sync(0xffffffffu, !(rs <= 0x1p64f))) {  // rare (also catches inf / NaN): own max
+          m_c = fmaxf(m_c, ceilf(fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2));
+          rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_c, pa);
+          rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_c, pa + 16);
+          rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_c, pb);
+          rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_c, pb + 16);
+        }
+        float m_fin = m_c;
+        if (j >= 1) {
+          ptx::mbar_wait(&m_ready[g4 * 2 + ((g - 1) & 1)], ((g - 1) >> 1) & 1);
+          stamp(p, g, 3);
+          const float m_prev = m_pub[((g - 1) & 1) * kRows + row_in_tile];
+          const float d = m_c - m_prev;
+          const bool move = d > kMoveThresh;
+          m_fin = move ? m_c : m_prev;
+          if (__any_sync(0xffffffffu, d != 0.f)) {  // unit's second tile, or after a rare move
+            if (__any_sync(0xffffffffu, move)) {  // O *= 2^(m_prev - m_c) once PV(g-1) is in
+              const float alpha = move ? ldexpf(1.f, int(m_prev - m_c)) : 1.f;
+              ptx::mbar_wait_cluster(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+              ptx::tc_fence_after();
+              scale_o<D>(tO, alpha);
+            }
+            const float beta = move ? 1.f : ldexpf(1.f, int(d));  // exact (flushes below 2^-149)
+            scale_bf16x2(pa, beta);
+            scale_bf16x2(pb, beta);
+            rs *= beta;
+          }
+        }
+        m_pub[(g & 1) * kRows + row_in_tile] = m_fin;
+        ptx::mbar_arrive(&m_ready[g4 * 2 + (g & 1)]);  // all 32 lanes (count 32)
+        if (g >= 2) ptx::mbar_wait_cluster(&pv_done[c], ((g - 2) >> 1) & 1);  // P[c] free again
+        stamp(p, g, 5);
+        ptx::tc_fence_after();
+        ptx::tmem_st32(tP, pa);       // keys 0..63
+        ptx::tmem_st32(tP + 32, pb);  // keys 64..127
+        if (m_fin != m_ref) {
+          l *= ptx::ex2(m_ref - m_fin);  // 0 * 0 on this warp's first step of the unit
+          m_ref = m_fin;
+        }
+        l += rs;
+        m_own = m_fin;
+        } else {
         uint32_t pk[32];
         const uint32_t tP = tmem + lane_off + C::col_p(c);
         auto exp2x = [&](const uint32_t (&a)[32], int col0, uint32_t* pko) -> float {
@@ -691,6 +745,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         }
         l += rs;
         m_own = m_fin;
+        }
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         __syncwarp();
