@@ -13,7 +13,16 @@ import os
 from typing import Optional, Sequence, Tuple
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("XDIT_LIB") or os.path.join(HERE, "libxdit_usp.so")  # XDIT_LIB: A/B builds
+LIB_PATH = os.path.join(HERE, "libxdit_usp.so")
+# Same-session kernel A/Bs (tools/ab_attn.sh) load a tagged build of this same source,
+# paper_2411_01738_b200/libxdit_usp_<tag>.so (python -m paper_2411_01738_b200.build --tag=...), by
+# XDIT_LIB; nothing else is accepted.
+_ab = os.environ.get("XDIT_LIB")
+if _ab:
+    _ab = os.path.abspath(_ab)
+    if os.path.dirname(_ab) != HERE or not os.path.basename(_ab).startswith("libxdit_usp_"):
+        raise ImportError(f"XDIT_LIB={_ab}: only tagged builds paper_2411_01738_b200/libxdit_usp_<tag>.so")
+    LIB_PATH = _ab
 
 ABI_VERSION = 30000  # XDIT_ABI_VERSION of include/xdit_usp.h
 XDIT_STATUS = {0: "OK", 1: "INVALID_ARG", 2: "UNSUPPORTED", 3: "DIVISIBILITY", 4: "COMM_MISMATCH",
