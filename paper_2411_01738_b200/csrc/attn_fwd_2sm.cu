@@ -60,7 +60,6 @@ constexpr int kRows = 128;         // query rows per CTA (= TMEM lanes)
 constexpr int kKeys = 128;         // keys per step
 constexpr float kMoveThresh = 40.0f;    // log2 units: a reference jump above 2^40 moves it (R1')
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kRegsSoftmax = 216, kRegsOther = 72;  // setmaxnreg split of 384 x 168 registers
 constexpr int kRing = 8;           // work-unit broadcast ring depth (units in flight <= 5, see below)
 // exp2 pairs (of every 8) the softmax evaluates with the FMA-pipe polynomial instead of MUFU.EX2:
 // 1 (same-session A/B with the deferred reconciliation, profiles/r02_ab_softmax.txt: +1-4 % over 0
@@ -107,7 +106,13 @@ struct Cfg {
   static constexpr int kOW = kNPV + (kTail ? 32 : 0);    // O columns in TMEM
   static constexpr int kStageBytes = ((kKBytes > kVBytes ? kKBytes : kVBytes) + 1023) / 1024 * 1024;
   // even: K in even stages, V in odd; D = 128 keeps 8 (4 key tiles) so the double-buffered Q fits
-  static constexpr int kStages = D == 128 ? 8 : (D == 64 ? 20 : 14);
+  static constexpr int kStages = D == 128 ? 9 : (D == 64 ? 20 : 14);
+  // Per-head-dim tuning (same-session A/Bs, profiles/r02_ab_tuning_d128.txt): at D = 128 one exp2
+  // pair in 16 on the FMA pipe (1 in 8 at D = 64 / 72) and 224 registers for the softmax warps
+  // (setmaxnreg split 256 x R + 128 x R' = 64512 of the 384 x 168 at launch).
+  static constexpr int kEmuPeriod = D == 128 ? 16 : 8;
+  static constexpr uint32_t kRegsSoftmax = D == 128 ? 224 : 216;
+  static constexpr uint32_t kRegsOther = (64512u - 256u * kRegsSoftmax) / 128u;
   static constexpr int kSmemBar = 1024;
   static constexpr int kQRegion = (kQBytes + 1023) / 1024 * 1024;
   static constexpr int kSmemBytes = 2 * kQRegion + kStages * kStageBytes + kSmemBar + 1024;
@@ -202,8 +207,8 @@ __device__ __forceinline__ float max64(const uint32_t (&a)[32], const uint32_t (
 
 // P = exp2(S * sl2 - m) for 32 of this warp's columns (col0: their first column within the warp's
 // 64, for the ragged-tail mask) into 16 packed bf16x2 registers; returns the fp32 row sum of P.
-// EMU of every 8 column pairs use the FMA-pipe polynomial (exp2_poly2) instead of MUFU.EX2.
-template <bool MASK, int EMU>
+// EMU of every PERIOD column pairs use the FMA-pipe polynomial (exp2_poly2) instead of MUFU.EX2.
+template <bool MASK, int EMU, int PERIOD = 8>
 __device__ __forceinline__ float exp_pack32(const uint32_t (&a)[32], int col0, int valid, float sl2,
                                             float neg_m, uint32_t* pk) {
   const uint64_t sc2 = pk2(sl2, sl2), nm2 = pk2(neg_m, neg_m);
@@ -213,7 +218,7 @@ __device__ __forceinline__ float exp_pack32(const uint32_t (&a)[32], int col0, i
     const int col = col0 + 2 * i;
     const uint64_t x = fma2(pk2(u2f(a[2 * i]), u2f(a[2 * i + 1])), sc2, nm2);
     float p0, p1;
-    if (!MASK && (i & 7) < EMU) {
+    if (!MASK && (i % PERIOD) < EMU) {
       up2(exp2_poly2(x), p0, p1);
     } else {
       float x0, x1;
@@ -374,7 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= 8) {
-   ptx::setmaxnreg_dec<kRegsOther>();
+   ptx::setmaxnreg_dec<C::kRegsOther>();
    if (warp == kWarpTma) {
     // ===================================================== TMA producer (both CTAs)
     // The leader's lane 0 also hands out the units: the t-th unit of this pair is fetched when the
@@ -553,7 +558,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
    }
   } else {
-    ptx::setmaxnreg_inc<kRegsSoftmax>();
+    ptx::setmaxnreg_inc<C::kRegsSoftmax>();
     // ===================================================== softmax (8 warps per CTA)
     // Warp w owns TMEM lanes / query rows 32 (w%4) .. +31 and the key tiles g = w/4 (mod 2) of the
     // pair's tile stream: the two warps of a lane quarter alternate steps, so one runs its exp2
@@ -641,17 +646,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if constexpr (D == 128) {
         uint32_t pa[32], pb[32];
         const uint32_t tP = tmem + lane_off + C::col_p(c);
-        float rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_c, pa);
-        rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_c, pa + 16);
+        float rs = exp_pack32<false, EMU, C::kEmuPeriod>(s0, 0, valid, sl2, -m_c, pa);
+        rs += exp_pack32<false, EMU, C::kEmuPeriod>(s1, 32, valid, sl2, -m_c, pa + 16);
         stamp(p, g, 4);
-        rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_c, pb);
-        rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_c, pb + 16);
+        rs += exp_pack32<false, EMU, C::kEmuPeriod>(s2, 64, valid, sl2, -m_c, pb);
+        rs += exp_pack32<false, EMU, C::kEmuPeriod>(s3, 96, valid, sl2, -m_c, pb + 16);
         if (__any_sync(0xffffffffu, !(rs <= 0x1p64f))) {  // rare (also catches inf / NaN): own max
           m_c = fmaxf(m_c, ceilf(fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2));
-          rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_c, pa);
-          rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_c, pa + 16);
-          rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_c, pb);
-          rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_c, pb + 16);
+          rs = exp_pack32<false, EMU, C::kEmuPeriod>(s0, 0, valid, sl2, -m_c, pa);
+          rs += exp_pack32<false, EMU, C::kEmuPeriod>(s1, 32, valid, sl2, -m_c, pa + 16);
+          rs += exp_pack32<false, EMU, C::kEmuPeriod>(s2, 64, valid, sl2, -m_c, pb);
+          rs += exp_pack32<false, EMU, C::kEmuPeriod>(s3, 96, valid, sl2, -m_c, pb + 16);
         }
         float m_fin = m_c;
         if (j >= 1) {
@@ -691,7 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         uint32_t pk[32];
         const uint32_t tP = tmem + lane_off + C::col_p(c);
         auto exp2x = [&](const uint32_t (&a)[32], int col0, uint32_t* pko) -> float {
-          return exp_pack32<false, EMU>(a, col0, valid, sl2, -m_c, pko);
+          return exp_pack32<false, EMU, C::kEmuPeriod>(a, col0, valid, sl2, -m_c, pko);
         };
         float rs = exp2x(s0, 0, pk);
         rs += exp2x(s1, 32, pk + 16);
@@ -704,11 +709,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         rs += exp2x(s3, 96, pk + 16);
         if (__any_sync(0xffffffffu, !(rs <= 0x1p64f))) {  // rare (also catches inf / NaN): own max
           m_c = fmaxf(m_c, ceilf(fmaxf(max64<false>(s0, s1, 64), max64<false>(s2, s3, 64)) * sl2));
-          rs = exp_pack32<false, EMU>(s0, 0, valid, sl2, -m_c, pk);
-          rs += exp_pack32<false, EMU>(s1, 32, valid, sl2, -m_c, pk + 16);
+          rs = exp_pack32<false, EMU, C::kEmuPeriod>(s0, 0, valid, sl2, -m_c, pk);
+          rs += exp_pack32<false, EMU, C::kEmuPeriod>(s1, 32, valid, sl2, -m_c, pk + 16);
           ptx::tmem_st32(tP, pk);
-          rs += exp_pack32<false, EMU>(s2, 64, valid, sl2, -m_c, pk);
-          rs += exp_pack32<false, EMU>(s3, 96, valid, sl2, -m_c, pk + 16);
+          rs += exp_pack32<false, EMU, C::kEmuPeriod>(s2, 64, valid, sl2, -m_c, pk);
+          rs += exp_pack32<false, EMU, C::kEmuPeriod>(s3, 96, valid, sl2, -m_c, pk + 16);
         }
         float m_fin = m_c;
         if (j >= 1) {
