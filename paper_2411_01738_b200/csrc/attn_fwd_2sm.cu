@@ -106,12 +106,25 @@ struct Cfg {
   static constexpr int kOW = kNPV + (kTail ? 32 : 0);    // O columns in TMEM
   static constexpr int kStageBytes = ((kKBytes > kVBytes ? kKBytes : kVBytes) + 1023) / 1024 * 1024;
   // even: K in even stages, V in odd; D = 128 keeps 8 (4 key tiles) so the double-buffered Q fits
+#ifdef XDIT_T_STAGES  // A/B builds: override the per-head-dim tuning below
+  static constexpr int kStages = D == 128 ? 9 : XDIT_T_STAGES;
+#else
   static constexpr int kStages = D == 128 ? 9 : (D == 64 ? 20 : 14);
-  // Per-head-dim tuning (same-session A/Bs, profiles/r02_ab_tuning_d128.txt): at D = 128 one exp2
-  // pair in 16 on the FMA pipe (1 in 8 at D = 64 / 72) and 224 registers for the softmax warps
-  // (setmaxnreg split 256 x R + 128 x R' = 64512 of the 384 x 168 at launch).
+#endif
+  // Per-head-dim tuning (same-session A/Bs, profiles/r02_ab_tuning_d128.txt, r02_ab_tuning_d64_d72.txt):
+  // at D = 128 one exp2 pair in 16 on the FMA pipe (1 in 8 at D = 64 / 72); softmax warps get 224
+  // registers at D = 128, 208 at D = 64 (more for the TMA / MMA warps), 216 at D = 72 (setmaxnreg
+  // split 256 x R + 128 x R' = 64512 of the 384 x 168 at launch).
+#ifdef XDIT_T_EMUP
+  static constexpr int kEmuPeriod = XDIT_T_EMUP;
+#else
   static constexpr int kEmuPeriod = D == 128 ? 16 : 8;
-  static constexpr uint32_t kRegsSoftmax = D == 128 ? 224 : 216;
+#endif
+#ifdef XDIT_T_REGS
+  static constexpr uint32_t kRegsSoftmax = XDIT_T_REGS;
+#else
+  static constexpr uint32_t kRegsSoftmax = D == 128 ? 224 : (D == 64 ? 208 : 216);
+#endif
   static constexpr uint32_t kRegsOther = (64512u - 256u * kRegsSoftmax) / 128u;
   static constexpr int kSmemBar = 1024;
   static constexpr int kQRegion = (kQBytes + 1023) / 1024 * 1024;
