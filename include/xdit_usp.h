@@ -301,10 +301,14 @@ typedef struct xdit_rowmap {
  * (D in {64,72,128}; q,k,v 16-byte aligned, strides multiples of 8 elements), 1 = fp32 inputs on the
  * SIMT kernel (D in [1,256]).  out_f32: 0 writes O as bf16 through `omap` (final output);
  * 1 writes O as fp32 through `omap` (ring partial).  lse may be NULL (skipped).
- * scratch: optional 16-byte aligned DEVICE buffer of scratch_bytes (>= xdit_attn_scratch_bytes(D)
- * to be used) that lets the bf16 kernel split the last, partial wave of its grid over key ranges
- * (merged by an LSE-weighted tail kernel); NULL runs every work item over all keys.  Results are
- * the same within rounding either way.
+ * The bf16 kernel is persistent: one CTA pair per TPC loops over work units (256 query rows of one
+ * (b, h) against a key range).  scratch: optional 16-byte aligned DEVICE buffer of scratch_bytes
+ * (>= xdit_attn_scratch_bytes(D) to be used), owned by the caller and not shared with a concurrent
+ * launch; with it the kernel hands the units out through an atomic counter at the buffer's end
+ * (reset by a 4-byte memset on `stream` before the launch) and splits the last, partial round of
+ * units over key ranges (merged by an LSE-weighted tail kernel); NULL hands the units out
+ * round-robin and runs every unit over all keys.  Results are the same within rounding either way
+ * (bitwise the same when no tail split applies).
  * Errors: INVALID_ARG, UNSUPPORTED, ALIGNMENT, CUDA. */
 XDIT_API int xdit_attn_fwd(const void* q, const void* k, const void* v, void* o, float* lse, int B, int H,
                   int Sq, int Skv, int D, int64_t q_b, int64_t q_s, int64_t q_h, int64_t kv_b,

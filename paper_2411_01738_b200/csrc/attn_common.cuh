@@ -1,6 +1,6 @@
-// attn_common.cuh -- pieces shared by the two bf16 attention kernels (attn_fwd_sm100.cu: one CTA
-// per query-tile pair; attn_fwd_2sm.cu: a CTA pair on one TPC): epilogue parameters, packed fp32x2
-// helpers, the FMA-pipe exp2, the tail-split merge kernel and the TMA tensor-map encoder.
+// attn_common.cuh -- pieces of the bf16 attention kernel (attn_fwd_2sm.cu: persistent CTA pairs)
+// kept apart from it: epilogue parameters, packed fp32x2 helpers, the FMA-pipe exp2, the tail-split
+// merge kernel and the TMA tensor-map encoder.
 #pragma once
 #include <cuda.h>
 #include <cudaTypedefs.h>
