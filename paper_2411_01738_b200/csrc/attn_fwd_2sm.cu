@@ -781,8 +781,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       l = xsum[row_in_tile] * ptx::ex2(xref[row_in_tile] - m_used) +
           xsum[kRows + row_in_tile] * ptx::ex2(xref[kRows + row_in_tile] - m_used);
       ptx::named_bar_sync(1 + g4, 64);  // xsum / xref / m_pub read: the next unit may rewrite them
+      if (c != int(glast & 1u)) stamp(p, glast, 0);  // profiling: epilogue phases (warp not on the last tile)
       // O out of TMEM into registers, then hand TMEM's O to the next unit's first P.V
       ptx::mbar_wait_cluster(o_full, t & 1);
+      if (c != int(glast & 1u)) stamp(p, glast, 1);  // profiling: epilogue phases (warp not on the last tile)
       ptx::tc_fence_after();
       uint32_t o[C::kOChunks][32];
       uint32_t o8[8];
@@ -791,9 +793,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         if (c * 32 + 64 * k < (D / 32) * 32) ptx::tmem_ld32(tO + c * 32 + 64 * k, o[k]);
       if (D % 32 && c == 0) ptx::tmem_ld8(tO + (D / 32) * 32, o8);
       ptx::tmem_ld_wait();
+      if (c != int(glast & 1u)) stamp(p, glast, 2);  // profiling: epilogue phases (warp not on the last tile)
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(o_empty_cl);
+      if (c != int(glast & 1u)) stamp(p, glast, 3);  // profiling: epilogue phases (warp not on the last tile)
       const int row = U.m0 + row_in_tile;
       const float inv_l = 1.f / l;
       RowDst dst = rowmap_dst(p.map, U.b, row, U.h);
@@ -849,6 +853,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       if (c == 0 && valid_row && lbase)
         lbase[dst.l_off] = U.piece >= 0 ? (m_used + log2f(l)) * 0.69314718055994530942f : lse_row;
       gbase += uint32_t(n_kv);
+      if (c != int(glast & 1u)) stamp(p, glast, 5);  // profiling: epilogue phases (warp not on the last tile)
     }
   }
   __syncwarp();
