@@ -205,6 +205,23 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def clock_ceilings(D: int, sm_mhz, n_sm: int, achieved: float):
+    """The kernel's two unit ceilings at the clock the run actually held ("report the
+    exp-limited ceiling beside the achieved fraction"): the tensor pipe (8192 dense bf16 FLOP per clock
+    per SM) and the MUFU (16 ex2 per clock per SM; one exp2 per 4D FLOPs, the FMA-pipe offload of
+    attn_fwd_2sm.cu -- 1 pair in 16 at D = 128, 1 in 8 below -- taken off it).  DESIGN.md 7.1b."""
+    if not sm_mhz:
+        return None
+    hz = float(sm_mhz) * 1e6
+    f_fma = 1.0 / 16 if D == 128 else 1.0 / 8
+    tensor = 8192.0 * n_sm * hz / 1e12
+    mufu = 16.0 * n_sm * hz * 4 * D / (1.0 - f_fma) / 1e12
+    binding = "mufu" if mufu < tensor else "tensor"
+    return {"sm_mhz": sm_mhz, "tensor_tflops_at_clock": tensor, "mufu_exp2_tflops_at_clock": mufu,
+            "exp2_on_fma_pipe": f_fma, "binding": binding,
+            "frac_of_binding": achieved / min(tensor, mufu)}
+
+
 # ------------------------------------------------------------------------------------ CPU oracle
 def cpu_baseline_leg(w, seconds: float, q_rows, k_heads, v_heads, rows_desc: str, got=None):
     """The cpu_baseline leg: the fp64 oracle, as it stands, on the host cores, on a bounded sample of
@@ -635,6 +652,9 @@ def main(argv=None):
             "cpu_baseline": cpu,
             "clocks": clocks.summary(),
         }
+        line["roofline"]["ceilings"] = clock_ceilings(w.D, line["clocks"].get("sm_mhz"),
+                                                      torch.cuda.get_device_properties(dev).multi_processor_count,
+                                                      kern_tflops)
         if N > 1:
             line["comm"] = comm_summary(pl, B, w, u, r, ms)
             line["phases"] = phases

@@ -68,3 +68,18 @@ def test_comm_bytes_match_table1():
         got = bench.comm_summary(pl, w.B, w, u, r, 1.0)["bytes_per_rank"]
         assert abs(got - mb) / mb < 0.01, (u, r, got, mb)
     assert bench.comm_summary(usp.plan(1, 24, 512, 65536, 128, 1, 1, 0), 1, w, 1, 1, 1.0) is None
+
+
+def test_clock_ceilings():
+    """The unit ceilings the bench prints beside the achieved fraction: at D = 64 the
+    MUFU binds (16 ex2/clk/SM, one exp2 per 4D FLOPs, 1/8 of them on the FMA pipe), at D = 128 the
+    tensor pipe (8192 FLOP/clk/SM) -- both scale with the clock the run held."""
+    import bench
+    c = bench.clock_ceilings(64, 1000, 100, 100.0)
+    assert c["binding"] == "mufu"
+    assert abs(c["mufu_exp2_tflops_at_clock"] - 16 * 100 * 1e9 * 256 / (7 / 8) / 1e12) < 1e-9
+    assert abs(c["tensor_tflops_at_clock"] - 8192 * 100 * 1e9 / 1e12) < 1e-9
+    assert abs(c["frac_of_binding"] - 100.0 / c["mufu_exp2_tflops_at_clock"]) < 1e-12
+    c = bench.clock_ceilings(128, 1000, 100, 100.0)
+    assert c["binding"] == "tensor" and c["exp2_on_fma_pipe"] == 1 / 16
+    assert bench.clock_ceilings(64, None, 100, 1.0) is None
