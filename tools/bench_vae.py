@@ -38,6 +38,6 @@ for (H, W, Ci, Co, act) in [(128, 128, 512, 512, 1), (256, 256, 256, 256, 1), (5
     wt, bd = dec.layers[0]
     ext_t = torch.randn(H + 2, W, Ci, device="cuda").to(torch.bfloat16)
     ms = timeit(lambda: vae.conv(ext_t, wt, bd, bool(act)), iters=20)
-    print(json.dumps({"kernel": "vae_conv_tc_kernel", "dtype": "bf16", "shape": {"H": H, "W": W, "Ci": Ci, "Co": Co, "act_up": act},
+    print(json.dumps({"kernel": "vae_conv_tcp_kernel", "dtype": "bf16", "shape": {"H": H, "W": W, "Ci": Ci, "Co": Co, "act_up": act},
                       "ms": ms, "tflops": fl / ms / 1e9, "roofline": {"bound": "tensor", "peak": bf16_peak, "unit": "TFLOP/s",
                       "peak_source": "measured bf16 burst (MEASURED_PEAKS.json bf16_tflops)", "frac": fl / ms / 1e9 / bf16_peak}}), flush=True)
