@@ -3,16 +3,18 @@
 //
 // out[y][x][co] = b[co] + sum_{dy,dx} sum_ci w[co][ci][dy][dx] * in[y+dy][x+dx-1][ci]
 // over a halo-extended row band in[H+2][W][Ci] (bf16, channels innermost), zero padding in x.
-// GEMM view per (tap, 64-channel chunk): A = 128 consecutive pixels of one input row, shifted by the
-// tap (TMA box (64 ch, 128 px) at (ci0, row y+dy, x0+dx-1); out-of-range pixels and channels are
-// zero-filled by the TMA, which IS the zero padding), B = the tap's weights for COT output channels
-// (wt[9][Co][Ci], K-major), D = pixels x COT channels in TMEM (fp32), accumulated over 9 taps x
-// ceil(Ci/64) chunks, 4 MMAs (K = 16) each.  CTA PAIRS (cta_group::2, M = 256): a 2-CTA cluster
-// takes output rows y, y+1 of one 128-pixel strip and COT (128 or 256) output channels; each CTA
-// loads its own pixel tile and HALF of the weights.  Warp 4 = TMA producer (both CTAs), warp 5 = MMA
-// issuer (leader), warps 0-3 = epilogue (thread = pixel = TMEM lane): bias, optional SiLU + nearest
-// x2 upsample, bf16 [H'][W'][Co8] (Co rounded up to 8, the extra channels zero) written through
-// shared memory with TMA stores.
+// GEMM view: A = 128 consecutive pixels of input row y+dy shifted by dx-1, B = tap (dy, dx)'s weights
+// for COT output channels (wt[9][Co][Ci], K-major), D = pixels x COT channels in TMEM (fp32),
+// accumulated over 3 dy x ceil(Ci/64) channel chunks x 3 dx x 4 MMAs (K = 16).  One TMA box of 136
+// pixels x 64 channels at (ci0, row y+dy, x0-1) serves all three dx taps (the shift is a 128-byte
+// offset of the MMA descriptor into the 128B-swizzled tile); out-of-range pixels and channels are
+// zero-filled by the TMA, which IS the zero padding.  CTA PAIRS (cta_group::2, M = 256): a 2-CTA
+// cluster takes output rows y, y+1 of one 128-pixel strip and COT (128 or 256) output channels; each
+// CTA loads its own pixel row and HALF of the weights.  Persistent: one cluster per TPC loops over
+// the tiles, two TMEM accumulators.  Warp 4 = TMA producer (both CTAs), warp 5 = MMA issuer
+// (leader), warps 0-3 = epilogue (thread = pixel = TMEM lane): bias, optional SiLU + nearest x2
+// upsample, bf16 [H'][W'][Co8] (Co rounded up to 8, the extra channels zero) written through shared
+// memory with TMA stores.
 // Every pixel's sum is the same MMA sequence whatever band it sits in, so the banded decode stays
 // bit-identical to the whole-image decode.
 #include <cuda.h>
@@ -30,7 +32,6 @@ namespace xdit {
 namespace {
 
 constexpr int kPix = 128, kKC = 64;
-constexpr int kTileA = kPix * kKC * 2;  // 16 KB
 // TMA store of a 4-D box from shared memory (bulk-group completion) and its helpers.
 __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2,
                                              int c3) {
@@ -58,8 +59,14 @@ template <int COT>
 struct TCP {
   static constexpr int kCoT = COT, kCoHalf = COT / 2;
   static constexpr int kTileB = kCoHalf * kKC * 2;
-  static constexpr int kStageBytes = kTileA + kTileB;
-  static constexpr int kStages = COT == 256 ? 6 : 8;
+  // one pixel row per (dy, channel chunk) for all three dx taps: 136 pixels (x0-1 .. x0+134) and the
+  // three taps' weight halves in one stage; the dx shift is a 128-byte start offset into the
+  // 128B-swizzled pixel tile (the swizzle follows the absolute smem address bits, so the shifted
+  // descriptor needs no base offset -- with base offset dx the parity tests fail)
+  static constexpr int kRowsA = 136;
+  static constexpr int kTileAX = kRowsA * kKC * 2;
+  static constexpr int kStageBytes = (kTileAX + 1023) / 1024 * 1024 + 3 * kTileB;
+  static constexpr int kStages = COT == 256 ? 3 : 4;
   static constexpr int kOutBytes = 2 * kPix * 64;  // 256 staging rows of 32 bf16 channels
   static constexpr int kSmem = kStages * kStageBytes + kOutBytes + 1024 + 256;
 };
@@ -81,7 +88,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = ptx::cluster_ctarank();
-  const int nkc = (Ci + kKC - 1) / kKC, nk = 9 * nkc;
+  const int nkc = (Ci + kKC - 1) / kKC;
   const int n_sx = (W + kPix - 1) / kPix, n_by = (Hout + 1) / 2, n_z = (Co + kCoT - 1) / kCoT;
   const int n_tiles = n_sx * n_by * n_z;
   const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -119,16 +126,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
       for (int t = cid; t < n_tiles; t += ncl) {
         int x0, y, co0;
         tile(t, x0, y, co0);
-        for (int k = 0; k < nk; ++k, ++it) {
+        for (int k = 0; k < 3 * nkc; ++k, ++it) {  // (dy, chunk); the stage holds all three dx taps
           const int s = int(it % kStages);
           const uint32_t round = it / kStages;
           if (round > 0) ptx::mbar_wait(&empty[s], (round - 1) & 1);
-          const int tap = k / nkc, c0 = (k % nkc) * kKC, dy = tap / 3, dx = tap % 3;
-          if (rank == 0) ptx::mbar_expect_tx(&full[s], 2 * kStageBytes);
+          const int dy = k / nkc, c0 = (k % nkc) * kKC;
+          if (rank == 0) ptx::mbar_expect_tx(&full[s], 2 * (T::kTileAX + 3 * T::kTileB));
           const uint32_t full_cl = ptx::mapa(&full[s], 0);
           uint8_t* st = smem + s * kStageBytes;
-          ptx::tma_load_4d_pair(st, &tmX, full_cl, c0, y + dy, x0 + dx - 1, 0, pol);
-          ptx::tma_load_4d_pair(st + kTileA, &tmW, full_cl, c0, tap, co0 + int(rank) * T::kCoHalf, 0, pol);
+          ptx::tma_load_4d_pair(st, &tmX, full_cl, c0, y + dy, x0 - 1, 0, pol);
+          uint8_t* sb = st + (T::kTileAX + 1023) / 1024 * 1024;
+          for (int dx = 0; dx < 3; ++dx)
+            ptx::tma_load_4d_pair(sb + dx * T::kTileB, &tmW, full_cl, c0, 3 * dy + dx,
+                                  co0 + int(rank) * T::kCoHalf, 0, pol);
         }
       }
     }
@@ -142,18 +152,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(192, 1)
         const int ab = li & 1;
         if (li >= 2) ptx::mbar_wait(&acc_empty[ab], ((li - 2) >> 1) & 1);
         const uint32_t d = tmem + uint32_t(ab * kCoT);
-        for (int k = 0; k < nk; ++k, ++it) {
+        for (int k = 0; k < 3 * nkc; ++k, ++it) {
           const int s = int(it % kStages);
           ptx::mbar_wait(&full[s], (it / kStages) & 1);
           ptx::tc_fence_after();
           if (ptx::elect_one()) {
-            const uint32_t a = sa + s * kStageBytes, b = a + kTileA;
+            const uint32_t a = sa + s * kStageBytes, b = a + (T::kTileAX + 1023) / 1024 * 1024;
 #pragma unroll
-            for (int kk = 0; kk < kKC / 16; ++kk)
-              ptx::mma_ss_pair(d, ptx::sdesc_sw128(a + kk * 32, 16, 1024), ptx::sdesc_sw128(b + kk * 32, 16, 1024),
-                               idesc, (k > 0 || kk > 0) ? 1u : 0u);
+            for (int dx = 0; dx < 3; ++dx)
+#pragma unroll
+              for (int kk = 0; kk < kKC / 16; ++kk)  // pixel rows dx .. dx + 127: base offset dx
+                ptx::mma_ss_pair(d, ptx::sdesc_sw128(a + dx * 128 + kk * 32, 16, 1024),
+                                 ptx::sdesc_sw128(b + dx * T::kTileB + kk * 32, 16, 1024), idesc,
+                                 (k > 0 || dx > 0 || kk > 0) ? 1u : 0u);
             ptx::tc_commit_pair(&empty[s]);
-            if (k == nk - 1) ptx::tc_commit_pair(&acc_full[ab]);
+            if (k == 3 * nkc - 1) ptx::tc_commit_pair(&acc_full[ab]);
           }
           __syncwarp();
         }
@@ -262,7 +275,8 @@ cudaError_t launch_vae_conv_tc(const void* in, int Hout, int Ci, int W, const vo
   CUtensorMap mx, mo;
   const int Co8 = (Co + 7) / 8 * 8;  // output channel stride (16-byte rows for the TMA store)
   // activations [Hout+2][W][Ci]: dims (Ci, rows->"H", pixels->"S"); box 64 channels x 128 pixels
-  if (!make_map(&mx, in, 1, W, Hout + 2, Ci, int64_t(Hout + 2) * W * Ci, Ci, int64_t(W) * Ci, kKC, kPix) ||
+  constexpr int kBoxPix = 136;  // x0-1 .. x0+134: the three dx taps of a 128-pixel strip
+  if (!make_map(&mx, in, 1, W, Hout + 2, Ci, int64_t(Hout + 2) * W * Ci, Ci, int64_t(W) * Ci, kKC, kBoxPix) ||
       // output [H'][W'][Co8]: boxes of 32 channels (64B swizzle) x 128 (256 upsampled) pixels x 1 row
       !make_map(&mo, out, 1, act_up ? 2 * W : W, act_up ? 2 * Hout : Hout, Co8,
                 int64_t(act_up ? 4 : 1) * Hout * W * Co8, Co8, int64_t(act_up ? 2 * W : W) * Co8, 32,
