@@ -51,10 +51,10 @@ __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.
 // step 16 KB of pixels + COT*64 B of weights instead of 16 KB + COT*128 B (the one-CTA kernel of
 // round 1 ran its 2 x 48 KB stages latency-bound: ncu tensor pipe 43 %, L2 28 % of peak).
 // Persistent: one cluster per TPC loops over the tiles (row pair, 128-pixel strip,
-// COT-channel block; round-robin), the operand ring runs on across tiles (6 / 8 stages at one CTA
-// per SM), and two TMEM accumulators let the epilogue of tile i (its own staging buffer) overlap
-// the K loop of tile i + 1: acc_full[b] (MMA -> epilogue, multicast) / acc_empty[b] (the 8
-// epilogue warps of the pair -> the leader's MMA warp).
+// COT-channel block; round-robin), the operand ring runs on across tiles (3 / 4 stages of one pixel
+// row + three taps' weights at one CTA per SM), and two TMEM accumulators let the epilogue of tile i
+// (its own staging buffer) overlap the K loop of tile i + 1: acc_full[b] (MMA -> epilogue,
+// multicast) / acc_empty[b] (the 8 epilogue warps of the pair -> the leader's MMA warp).
 template <int COT>
 struct TCP {
   static constexpr int kCoT = COT, kCoHalf = COT / 2;
