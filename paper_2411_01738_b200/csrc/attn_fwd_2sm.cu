@@ -35,7 +35,8 @@
 // behind a concurrent NCCL kernel of the ring's side stream -- simply take fewer units) or, without
 // scratch, round-robin; the leader's TMA warp fetches each unit id and broadcasts it through a small
 // smem ring into both CTAs.
-// TMEM per SM (512 columns): S[0] [0,128) S[1] [128,256) P[0] [256,320) P[1] [320,384) O [384,384+D).
+// TMEM per SM (512 columns): S[0] [0,128) S[1] [128,256) P[0] [256,320) P[1] [320,384) O [384,384+D);
+// at D = 64 also Q[0] [448,480) Q[1] [480,512) (QK^T reads Q from TMEM, copied in by tcgen05.cp).
 // Head dims 128, 72 and 64 (the V halves of D = 64 are 32 columns: 64-byte swizzled rows).
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -136,6 +137,12 @@ struct Cfg {
   __host__ __device__ static constexpr uint32_t col_p(int b) { return 256u + uint32_t(b) * 64u; }
   static constexpr uint32_t kColO = 384u;
   static_assert(kColO + kOW <= kTmemCols, "TMEM budget");
+  // D = 64: QK^T as a TS MMA -- the unit's Q copied into TMEM (columns 448 + 32 qb, double-buffered
+  // by unit parity; the only head dim where it fits beside S, P and O) by tcgen05.cp, so only K is
+  // read from shared memory (same-session A/B: CogVideoX +0.8 %, SD3 ±0, profiles/r02_s3_ab_qtmem.txt)
+  static constexpr bool kQT = D == 64;
+  __host__ __device__ static constexpr uint32_t col_q(int qb) { return 448u + uint32_t(qb) * 32u; }
+  static_assert(!kQT || col_q(1) + 32 <= kTmemCols, "TMEM budget (Q)");
   static_assert(kSmemBytes + 6 * 1024 <= 227 * 1024, "smem budget (dynamic + static)");
 };
 
@@ -477,7 +484,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         const uint64_t oq = uint64_t(uint32_t(qb * C::kQRegion) >> 4), ok = uint64_t(uint32_t(sK * C::kStageBytes) >> 4);
 #pragma unroll
         for (int k = 0; k < C::kDpK / 16; ++k) {
-          if (C::kTail && k == C::kN128 * 4)
+          if constexpr (C::kQT)
+            ptx::mma_ts_pair(tmem + C::col_s(jb), tmem + C::col_q(qb) + k * 8,
+                             dk0 + ok + uint64_t(((k >> 2) * C::kKHalfAtom + (k & 3) * 32) >> 4), idesc_qk,
+                             k > 0 ? 1u : 0u);
+          else if (C::kTail && k == C::kN128 * 4)
             ptx::mma_ss_pair(tmem + C::col_s(jb), dq16 + oq, dk16 + ok, idesc_qk, 1u);
           else
             ptx::mma_ss_pair(tmem + C::col_s(jb), dq0 + oq + uint64_t(((k >> 2) * C::kAtom + (k & 3) * 32) >> 4),
@@ -526,6 +537,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         stamp(p, c.g, 2);
         ptx::tc_fence_after();
         if (ptx::elect_one()) {
+          if (C::kQT && c.j == 0) {  // the unit's Q into TMEM (in issue order before its QK^T)
+#pragma unroll
+            for (int k = 0; k < D / 16; ++k)
+              ptx::tc_cp_pair_128x256b(tmem + C::col_q(qb) + k * 8,
+                                       dq0 + uint64_t(uint32_t(qb * C::kQRegion) >> 4) + uint64_t((k * 32) >> 4));
+          }
           qk(c.g & 1, sK, qb);
           ptx::tc_commit_pair(&s_full[c.g & 1]);
           ptx::tc_commit_pair(&kv_empty[sK]);

@@ -285,6 +285,12 @@ __device__ __forceinline__ void tma_load_4d_pair(void* smem_dst, const CUtensorM
       : "memory");
 }
 // TMEM of the pair: one warp of EACH CTA executes these collectively.
+// smem -> TMEM copy of the pair (leader only): 128 rows x 256 bits of each CTA's shared-memory
+// matrix (descriptor as for an MMA operand) into its TMEM lanes 0-127, 8 columns from taddr; runs in
+// issue order with the issuing thread's tcgen05.mma.
+__device__ __forceinline__ void tc_cp_pair_128x256b(uint32_t taddr, uint64_t src_desc) {
+  asm volatile("tcgen05.cp.cta_group::2.128x256b [%0], %1;" ::"r"(taddr), "l"(src_desc) : "memory");
+}
 __device__ __forceinline__ void tmem_alloc_pair(uint32_t* smem_result, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                    smem_u32(smem_result)),
